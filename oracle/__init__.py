@@ -1,0 +1,172 @@
+"""oracle -- plain CPU oracle for exact butterfly counting.
+
+TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and
+``bench.py``'s ``cpu_baseline`` / ``--impl reference`` leg may import it.  The
+product (``paper_1907_08607_b200``) never imports it, and it never imports the
+product.  The arithmetic lives in ``oracle.c`` (see its header for the paper
+passages each function follows); this file is ctypes marshalling plus the
+assembly of the per-side arrays.
+
+Pins (tests/test_oracle_pins.py): Fig. 1 golden values, K_{a,b} closed forms,
+brute force over 4-tuples, every bipartite graph up to 4x4, the integer-matmul
+identity, the trace identity tr(B^4), invariants, Fig. 2's wedge listing, and
+the wedge-count closed form.  No oracle function is "parity unpinned".
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+ORC_ERRORS = {1: "ERANGE", 2: "EDUP", 3: "ENOMEM", 4: "EOVERFLOW", 5: "EINVAL"}
+RANK_KINDS = {"side": 0, "approx_degree": 1, "degree": 2, "explicit": 3}
+
+
+class OracleError(RuntimeError):
+    pass
+
+
+def build(force: bool = False) -> str:
+    src = os.path.join(_HERE, "oracle.c")
+    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(src):
+        subprocess.check_call(["gcc", "-O2", "-fPIC", "-shared", "-o", _SO, src])
+    return _SO
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        build()
+        lib = ctypes.CDLL(_SO)
+        vp, u32p, u64p = ctypes.c_void_p, ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(ctypes.c_uint64)
+        lib.orc_build.argtypes = [ctypes.c_uint32, ctypes.c_uint32, u32p, ctypes.c_uint64,
+                                  ctypes.POINTER(vp)]
+        lib.orc_free.argtypes = [vp]
+        lib.orc_count.argtypes = [vp, ctypes.c_int, ctypes.c_uint32, ctypes.c_uint32, u64p, u64p,
+                                  u64p, u64p]
+        lib.orc_cheap_side.argtypes = [vp]
+        lib.orc_vertex.argtypes = [vp, ctypes.c_int, ctypes.c_uint32, u64p]
+        lib.orc_edge.argtypes = [vp, u32p, ctypes.c_uint64, u64p]
+        lib.orc_rank.argtypes = [vp, ctypes.c_int, u32p]
+        lib.orc_wedges.argtypes = [vp, u32p, u64p, u64p]
+        _lib = lib
+    return _lib
+
+
+def _p32(a):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)) if a is not None else None
+
+
+def _p64(a):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)) if a is not None else None
+
+
+def _check(rc):
+    if rc != 0:
+        raise OracleError(ORC_ERRORS.get(rc, str(rc)))
+
+
+class OracleGraph:
+    """Per-side sorted adjacency of a simple bipartite graph."""
+
+    def __init__(self, n_u: int, n_v: int, edges: np.ndarray):
+        self.lib = _load()
+        self.n_u, self.n_v = int(n_u), int(n_v)
+        self.edges = np.ascontiguousarray(edges, dtype=np.uint32).reshape(-1, 2)
+        self.m = self.edges.shape[0]
+        h = ctypes.c_void_p()
+        _check(self.lib.orc_build(self.n_u, self.n_v, _p32(self.edges), self.m, ctypes.byref(h)))
+        self.h = h
+
+    def close(self):
+        if self.h:
+            self.lib.orc_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    @property
+    def n(self):
+        return (self.n_u, self.n_v)
+
+    def cheap_side(self) -> int:
+        return int(self.lib.orc_cheap_side(self.h))
+
+    def count_range(self, X: int, x_lo: int, x_hi: int, vertex=True, edge=True):
+        """One shard: x in [x_lo, x_hi) of side X.  Returns (bx, by, be, sum_bx)."""
+        nX, nY = self.n[X], self.n[1 - X]
+        bx = np.zeros(nX, np.uint64) if vertex else None
+        by = np.zeros(nY, np.uint64) if vertex else None
+        be = np.zeros(self.m, np.uint64) if edge else None
+        s = ctypes.c_uint64(0)
+        _check(self.lib.orc_count(self.h, X, x_lo, x_hi, _p64(bx), _p64(by), _p64(be), ctypes.byref(s)))
+        return bx, by, be, int(s.value)
+
+    def count(self, side: int | None = None, vertex=True, edge=True):
+        """Exact counts.  Returns dict(total, b_u, b_v, b_e) (arrays None if not asked).
+        side: enumeration side X (None = cheap side)."""
+        X = self.cheap_side() if side is None else side
+        bx, by, be, s = self.count_range(X, 0, self.n[X], vertex, edge)
+        if s % 2:
+            raise OracleError("sum of b(x) over a side is odd")
+        b_u, b_v = (bx, by) if X == 0 else (by, bx)
+        return dict(total=s // 2, b_u=b_u, b_v=b_v, b_e=be, side=X)
+
+    def count_full(self):
+        """'Full mode': enumerate both sides literally and
+        require that they agree."""
+        a = self.count(side=0)
+        b = self.count(side=1)
+        for k in ("b_u", "b_v", "b_e"):
+            if not np.array_equal(a[k], b[k]):
+                raise OracleError(f"side-0 and side-1 enumerations disagree on {k}")
+        if a["total"] != b["total"]:
+            raise OracleError("side-0 and side-1 totals disagree")
+        return a
+
+    def vertex(self, side: int, x: int) -> int:
+        out = ctypes.c_uint64(0)
+        _check(self.lib.orc_vertex(self.h, side, x, ctypes.byref(out)))
+        return int(out.value)
+
+    def edge(self, e: int) -> int:
+        out = ctypes.c_uint64(0)
+        _check(self.lib.orc_edge(self.h, _p32(self.edges), e, ctypes.byref(out)))
+        return int(out.value)
+
+    def rank(self, kind: str, explicit: np.ndarray | None = None) -> np.ndarray:
+        """rank[gid] with gid = u or n_u + v (readings Z1-Z4)."""
+        n = self.n_u + self.n_v
+        r = np.zeros(max(n, 1), np.uint32) if explicit is None else np.ascontiguousarray(explicit, np.uint32).copy()
+        _check(self.lib.orc_rank(self.h, RANK_KINDS[kind], _p32(r)))
+        return r[:n]
+
+    def wedges(self, rank: np.ndarray):
+        """(W, w[gid]) under a ranking: Alg. 2's loop bounds."""
+        n = self.n_u + self.n_v
+        r = np.ascontiguousarray(rank, np.uint32)
+        w = np.zeros(max(n, 1), np.uint64)
+        t = ctypes.c_uint64(0)
+        _check(self.lib.orc_wedges(self.h, _p32(r), _p64(w), ctypes.byref(t)))
+        return int(t.value), w[:n]
+
+
+def count(n_u, n_v, edges, **kw):
+    with OracleGraph(n_u, n_v, edges) as g:
+        return g.count(**kw)
