@@ -1,0 +1,161 @@
+/*
+ * bf.h -- C ABI of libbf, B200-native exact butterfly counting.
+ *
+ * The operation: exact butterfly counts of a simple bipartite graph
+ * G = (U, V, E) (§2): the global count, the count per
+ * vertex (Eq. (1), on both sides) and the count per edge
+ * (Eq. (2)), computed by rank-ordered wedge retrieval and
+ * aggregation (Alg. 1 PREPROCESS P:639-657, Alg. 2 GET-WEDGES P:733-749,
+ * get-freq P:798-808, Alg. 3 COUNT-V P:821-844, Alg. 4 COUNT-E P:876-893).
+ *
+ * Conventions (all functions):
+ *  - extern "C", no exceptions cross the ABI; every call returns bf_status.
+ *  - On error, outputs are unspecified; the graph stays usable except after
+ *    BF_ECUDA / BF_ENCCL (then only bf_graph_destroy is valid).
+ *    bf_last_error() returns a message for the calling thread's last error.
+ *  - Ids are 0-based and side-local: u in [0, n_u), v in [0, n_v).
+ *  - Limits: n_u + n_v < 2^32, m < 2^31.  m = 0, n_u = 0, n_v = 0 are legal.
+ *  - All counts are exact uint64 (reading Z9); inputs must have < 2^64
+ *    butterflies (not checked unless BF_FLAG_CHECK_OVERFLOW).
+ *  - Threading: one host thread at a time per bf_graph.  Different graphs
+ *    (e.g. on different devices) may be used concurrently.
+ *  - Multi-GPU (bf_options.world_size > 1): every rank calls create, rank and
+ *    count with identical inputs; bf_count_* is collective over nccl_comm and
+ *    every rank receives the full result.
+ */
+#ifndef BF_H
+#define BF_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct bf_graph bf_graph; /* opaque; owns all device state */
+
+typedef enum {
+  BF_OK = 0,
+  BF_EINVAL = 1,     /* bad argument (NULL pointer, size over a limit, bad enum) */
+  BF_ERANGE = 2,     /* an edge id is out of range (u >= n_u or v >= n_v)        */
+  BF_EDUP = 3,       /* a (u,v) pair occurs twice: the graph must be simple      */
+  BF_ENOMEM = 4,     /* device or host allocation failed                        */
+  BF_ECUDA = 5,      /* a CUDA call failed (graph no longer usable)             */
+  BF_ENCCL = 6,      /* an NCCL call failed, or NCCL could not be loaded        */
+  BF_ENORANK = 7,    /* bf_count_* / bf_wedge_count called before bf_rank       */
+  BF_EOVERFLOW = 8   /* reserved: debug overflow check tripped                  */
+} bf_status;
+
+/* Vertex orderings (§3.1.1).  rank 0 is processed first
+ * as the low endpoint x1 of its wedges (reading Z4).
+ *  BF_RANK_SIDE          one whole side first: the side whose vertices, as
+ *                        endpoints, give fewer wedges, i.e. U first iff
+ *                        Σ_{v∈V} C(deg v,2) <= Σ_{u∈U} C(deg u,2) (reading Z1,
+ *                        tie -> U); within a side by id.
+ *  BF_RANK_APPROX_DEGREE decreasing floor(log2 deg), deg 0 last (reading Z3),
+ *                        ties by global id gid = u | n_u + v (reading Z2).
+ *  BF_RANK_DEGREE        decreasing degree, ties by gid (reading Z2).        */
+typedef enum { BF_RANK_SIDE = 0, BF_RANK_APPROX_DEGREE = 1, BF_RANK_DEGREE = 2 } bf_rank_kind;
+
+/* Wedge retrieval orientation.  Both retrieve exactly the same wedge set
+ * {(x1,y,x2): rank(y) > rank(x1), rank(x2) > rank(x1)} (Fig.
+ * fig:framework step 2), so every output is identical.
+ *  BF_ORIENT_LOW   Alg. 2 literally: iterate the lower-ranked endpoint x1,
+ *                  aggregate by x2.
+ *  BF_ORIENT_HIGH  the cache optimisation (§3.1.4; Wang et al.):
+ *                  iterate the higher-ranked endpoint x2, aggregate by x1.
+ *  BF_ORIENT_AUTO  library choice (currently HIGH).                          */
+typedef enum { BF_ORIENT_AUTO = 0, BF_ORIENT_LOW = 1, BF_ORIENT_HIGH = 2 } bf_orient;
+
+/* test_flags bits (path forcing for tests; 0 in production) */
+#define BF_FLAG_FORCE_WARP      0x1u  /* every start vertex on the warp-hash path     */
+#define BF_FLAG_FORCE_CTA       0x2u  /* every start vertex on the CTA path            */
+#define BF_FLAG_SMALL_WINDOW    0x4u  /* shrink the CTA's shared-memory key window so
+                                         most keys take the global-row path           */
+#define BF_FLAG_CHECK_OVERFLOW  0x8u  /* reserved                                      */
+
+typedef struct {
+  int device;               /* CUDA ordinal                                           */
+  void* stream;             /* cudaStream_t to run on; NULL = library-owned stream    */
+  void* nccl_comm;          /* ncclComm_t from bf_nccl_comm_create; NULL = 1 GPU      */
+  int world_rank;           /* this process's rank in [0, world_size)                 */
+  int world_size;           /* number of GPUs sharing the work (1 = single GPU)       */
+  int edges_on_device;      /* 1: `edges` in bf_graph_create is a device pointer      */
+  int outputs_on_device;    /* 1: output arrays of bf_count_* are device pointers     */
+  int orient;               /* bf_orient                                              */
+  uint32_t test_light_max_wedges; /* 0 = default warp-path threshold (wedges/start)   */
+  uint32_t test_flags;      /* BF_FLAG_* (tests only)                                 */
+  int virtual_world;        /* >1: single-GPU emulation of that many ranks: each
+                               virtual rank's share is counted in turn and the shares
+                               are summed on device, no NCCL (tests only)             */
+} bf_options;
+
+/* Fills *opt with defaults: device 0, library stream, 1 GPU, host pointers. */
+void bf_options_default(bf_options* opt);
+
+/* Copies the edge list to the device, range-checks it, rejects duplicates and
+ * computes degrees (§8(a) a1).  edges: m pairs (u, v), uint32, row-major
+ * [m][2]; host pointer unless opt->edges_on_device.  The caller keeps
+ * ownership of `edges` and may free it after the call returns.
+ * opt may be NULL (defaults).  *out receives the graph (NULL on error).
+ * Errors: BF_EINVAL (NULL out, size over limit), BF_ERANGE, BF_EDUP,
+ * BF_ENOMEM, BF_ECUDA. */
+bf_status bf_graph_create(uint32_t n_u, uint32_t n_v, const uint32_t* edges, uint64_t m,
+                          const bf_options* opt, bf_graph** out);
+
+/* Ranks the vertices (§8(a) a2), builds the ranked CSR of Alg. 1 (a3) and
+ * the per-start wedge counts and work plan (a4).  Deterministic and identical
+ * on every rank.  May be called again to re-rank.  Errors: BF_EINVAL (bad
+ * kind / NULL g), BF_ENOMEM, BF_ECUDA. */
+bf_status bf_rank(bf_graph* g, bf_rank_kind kind);
+
+/* Global butterfly count (P:487 footnote: Σ over endpoint pairs of C(d,2)).
+ * total: one uint64 (host, or device if outputs_on_device).
+ * Errors: BF_EINVAL, BF_ENORANK, BF_ECUDA, BF_ENCCL. */
+bf_status bf_count_total(bf_graph* g, uint64_t* total);
+
+/* Per-vertex counts (Alg. 3; Eq. (1)) for both sides.  out_u: n_u uint64,
+ * out_v: n_v uint64, indexed by input ids; total: nullable, one uint64.
+ * Errors as bf_count_total. */
+bf_status bf_count_vertex(bf_graph* g, uint64_t* out_u, uint64_t* out_v, uint64_t* total);
+
+/* Per-edge counts (Alg. 4; Eq. (2)).  out_e: m uint64 in INPUT edge order
+ * (reading Z7); total: nullable.  Errors as bf_count_total. */
+bf_status bf_count_edge(bf_graph* g, uint64_t* out_e, uint64_t* total);
+
+/* W = number of wedges processed under the current ranking,
+ * the work metric of wedges/s (reading Z10).  Host output.
+ * Errors: BF_EINVAL, BF_ENORANK. */
+bf_status bf_wedge_count(const bf_graph* g, uint64_t* w);
+
+/* Wall time (ms, CUDA events on the graph's stream) of the last
+ * bf_count_*'s counting kernels alone, and of its whole call.  Host outputs. */
+bf_status bf_last_timing(const bf_graph* g, float* kernel_ms, float* call_ms);
+
+/* Number of libbf kernel launches issued since the graph was created. */
+uint64_t bf_launch_count(const bf_graph* g);
+
+/* Debug/test export of the ranked CSR (device -> host copies).  Any pointer
+ * may be NULL.  rid_of_gid[n]: rank-space id of global id gid (U-side vertices
+ * occupy rid [0,n_u) in rank order, V-side [n_u, n) in rank order);
+ * off[n+1], nbr[2m], pos[2m] (index of the slot's source in N(dst)),
+ * hi[n] (deg_x(x)), wstart[n] (wedges started at each rid under the current
+ * orientation).  Errors: BF_EINVAL, BF_ENORANK, BF_ECUDA. */
+bf_status bf_export_csr(const bf_graph* g, uint32_t* rid_of_gid, uint32_t* off, uint32_t* nbr,
+                        uint32_t* pos, uint32_t* hi, uint64_t* wstart);
+
+/* NCCL bootstrap (the process group only carries the 128-byte id).  NCCL is
+ * loaded at run time (libnccl.so.2); BF_ENCCL if it cannot be loaded. */
+bf_status bf_nccl_unique_id(uint8_t id[128]);
+bf_status bf_nccl_comm_create(const uint8_t id[128], int rank, int world, int device, void** comm);
+bf_status bf_nccl_comm_destroy(void* comm);
+
+/* Frees all device state of g (NULL is a no-op). */
+void bf_graph_destroy(bf_graph* g);
+
+const char* bf_status_str(bf_status s);
+const char* bf_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BF_H */

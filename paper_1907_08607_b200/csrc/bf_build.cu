@@ -1,0 +1,405 @@
+// bf_build.cu -- ingest (§8(a) a1), ranking (a2), ranked CSR (a3, Alg. 1
+// PREPROCESS) and the per-start wedge counts + work plan
+// (a4, wedge-aware batching P:473-480).
+//
+// Rank space ("rid"): U-side vertices occupy rids [0, n_u) in rank order,
+// V-side vertices [n_u, n) in rank order.  Same-side rank comparisons are rid
+// comparisons; cross-side comparisons use rkey[rid] = (tier << 32) | gid,
+// whose order is the ranking's total order (readings Z1-Z4).  Every
+// neighbour list N(x) is sorted by decreasing rank (Alg. 1 line 7), i.e. by
+// decreasing rid, so deg_x(x) = hi[x] is a prefix length and
+// deg_{x1}(y) = pos[x1->y] = index of x1 in N(y) (the twin slot's index).
+#include "bf_internal.h"
+#include "bf_device.cuh"
+#include <algorithm>
+
+namespace {
+
+constexpr int TPB = 256;
+inline unsigned grid_for(size_t n, int sms) {
+  size_t g = (n + TPB - 1) / TPB;
+  size_t cap = (size_t)sms * 32;
+  if (g > cap) g = cap;
+  if (g == 0) g = 1;
+  return (unsigned)g;
+}
+
+// ---- a1 -----------------------------------------------------------------------
+__global__ void k_validate_degree(const uint32_t* __restrict__ e, uint64_t m, uint32_t nU, uint32_t nV,
+                                  uint32_t* __restrict__ deg, uint32_t* __restrict__ flags) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
+    uint2 uv = reinterpret_cast<const uint2*>(e)[i];
+    if (uv.x >= nU || uv.y >= nV) { atomicOr(flags, 1u); continue; }
+    atomicAdd(&deg[uv.x], 1u);
+    atomicAdd(&deg[(uint64_t)nU + uv.y], 1u);
+  }
+}
+
+// open-addressing set of keys u*nV+v+1 (0 = empty); a repeated key sets flag 2
+__global__ void k_dup_check(const uint32_t* __restrict__ e, uint64_t m, uint32_t nV,
+                            unsigned long long* __restrict__ table, uint64_t mask, uint32_t* __restrict__ flags) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
+    uint2 uv = reinterpret_cast<const uint2*>(e)[i];
+    unsigned long long key = (unsigned long long)uv.x * nV + uv.y + 1ull;
+    unsigned long long h = (key * 0x9E3779B97F4A7C15ull) >> 17;
+    for (;;) {
+      h &= mask;
+      unsigned long long old = atomicCAS(&table[h], 0ull, key);
+      if (old == 0ull) break;
+      if (old == key) { atomicOr(flags, 2u); break; }
+      h++;
+    }
+  }
+}
+
+// ---- a2 -----------------------------------------------------------------------
+__global__ void k_side_sums(const uint32_t* __restrict__ deg, uint64_t n, uint32_t nU,
+                            unsigned long long* __restrict__ sums /*[2]: wedges with U / V endpoints*/) {
+  __shared__ unsigned long long s[2];
+  if (threadIdx.x < 2) s[threadIdx.x] = 0;
+  __syncthreads();
+  unsigned long long a = 0, b = 0;
+  for (uint64_t z = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; z < n; z += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t c = choose2(deg[z]);
+    if (z < nU) b += c;  // centred at a U vertex: endpoints in V
+    else a += c;         // centred at a V vertex: endpoints in U
+  }
+  a = warp_sum(a);
+  b = warp_sum(b);
+  if ((threadIdx.x & 31) == 0) { atomicAdd(&s[0], a); atomicAdd(&s[1], b); }
+  __syncthreads();
+  if (threadIdx.x < 2) atomicAdd(&sums[threadIdx.x], s[threadIdx.x]);
+}
+
+// sort key (side bit 31 | tier) and rank key per gid
+__global__ void k_rank_keys(const uint32_t* __restrict__ deg, uint64_t n, uint32_t nU, int kind,
+                            const unsigned long long* __restrict__ sums, uint32_t* __restrict__ skey,
+                            uint32_t* __restrict__ iota, uint64_t* __restrict__ rkey_gid) {
+  int u_first = kind == BF_RANK_SIDE ? (sums[0] <= sums[1]) : 1;
+  for (uint64_t z = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; z < n; z += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t d = deg[z];
+    uint32_t side = z >= nU;
+    uint32_t tier;
+    if (kind == BF_RANK_DEGREE) tier = 0x7FFFFFFFu - d;                           // decreasing degree
+    else if (kind == BF_RANK_APPROX_DEGREE) tier = d ? 63u - (31u - __clz(d)) : 64u;  // decreasing floor(log2 d)
+    else tier = (side == 0) == (u_first != 0) ? 0u : 1u;                          // first side, then the other
+    skey[z] = (side << 31) | (kind == BF_RANK_SIDE ? 0u : tier);
+    iota[z] = (uint32_t)z;
+    rkey_gid[z] = ((uint64_t)tier << 32) | z;
+  }
+}
+
+__global__ void k_rid_maps(const uint32_t* __restrict__ gid_of_rid, uint64_t n, const uint32_t* __restrict__ deg,
+                           const uint64_t* __restrict__ rkey_gid, uint32_t* __restrict__ rid_of_gid,
+                           uint64_t* __restrict__ rkey, uint32_t* __restrict__ deg_rid) {
+  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < n; r += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t gd = gid_of_rid[r];
+    rid_of_gid[gd] = (uint32_t)r;
+    rkey[r] = rkey_gid[gd];
+    deg_rid[r] = deg[gd];
+  }
+}
+
+// ---- a3 -----------------------------------------------------------------------
+__global__ void k_slot_keys(const uint32_t* __restrict__ e, uint64_t m, uint32_t nU, uint64_t n, int B,
+                            const uint32_t* __restrict__ rid_of_gid, uint64_t* __restrict__ keys,
+                            uint32_t* __restrict__ vals) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
+    uint2 uv = reinterpret_cast<const uint2*>(e)[i];
+    uint64_t ru = rid_of_gid[uv.x], rv = rid_of_gid[(uint64_t)nU + uv.y];
+    keys[2 * i] = (ru << B) | (n - 1 - rv);  // src U: (rid asc, dst rid desc)
+    keys[2 * i + 1] = (rv << B) | (n - 1 - ru);
+    vals[2 * i] = (uint32_t)(2 * i);
+    vals[2 * i + 1] = (uint32_t)(2 * i + 1);
+  }
+}
+
+__global__ void k_slot_decode(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ vals, uint64_t S,
+                              uint64_t n, int B, uint32_t* __restrict__ nbr, uint32_t* __restrict__ src,
+                              uint32_t* __restrict__ where, uint32_t* __restrict__ slot_u, uint32_t* __restrict__ slot_v) {
+  uint64_t mask = (B >= 64) ? ~0ull : ((1ull << B) - 1);
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < S; j += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t k = keys[j];
+    uint32_t v = vals[j];
+    nbr[j] = (uint32_t)(n - 1 - (k & mask));
+    src[j] = (uint32_t)(k >> B);
+    where[v] = (uint32_t)j;
+    if (v & 1u) slot_v[v >> 1] = (uint32_t)j;
+    else slot_u[v >> 1] = (uint32_t)j;
+  }
+}
+
+__global__ void k_pos_hi(const uint32_t* __restrict__ vals, const uint32_t* __restrict__ where,
+                         const uint32_t* __restrict__ nbr, const uint32_t* __restrict__ src,
+                         const uint32_t* __restrict__ off, const uint64_t* __restrict__ rkey, uint64_t S,
+                         uint32_t* __restrict__ pos, uint32_t* __restrict__ hi) {
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < S; j += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t y = nbr[j], x = src[j];
+    uint32_t twin = where[vals[j] ^ 1u];
+    pos[j] = twin - off[y];
+    bool f = rkey[y] > rkey[x];
+    if (f) {
+      bool last = (j + 1 == off[x + 1]) || !(rkey[nbr[j + 1]] > rkey[x]);
+      if (last) hi[x] = (uint32_t)(j - off[x] + 1);
+    }
+  }
+}
+
+// per-slot wedge count under the orientation (a4)
+__global__ void k_wslot(const uint32_t* __restrict__ nbr, const uint32_t* __restrict__ src,
+                        const uint32_t* __restrict__ pos, const uint32_t* __restrict__ off,
+                        const uint32_t* __restrict__ hi, uint64_t S, int orient, uint32_t* __restrict__ wslot) {
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < S; j += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t x = src[j], y = nbr[j];
+    uint32_t w;
+    if (orient == BF_ORIENT_LOW) {
+      // Alg. 2: slot i < deg_x(x) retrieves N(y)[0 : deg_x(y)), deg_x(y) = pos
+      w = (j - off[x] < hi[x]) ? pos[j] : 0u;
+    } else {
+      // cache-optimised: x is the higher endpoint; y's neighbours ranked below
+      // both x and y: N(y)[max(hi[y], pos+1) : deg(y))
+      uint32_t d = off[y + 1] - off[y];
+      uint32_t st = max(hi[y], pos[j] + 1u);
+      w = d > st ? d - st : 0u;
+    }
+    wslot[j] = w;
+  }
+}
+
+__global__ void k_wstart(const uint64_t* __restrict__ wpre, const uint32_t* __restrict__ off, uint64_t n,
+                         uint64_t* __restrict__ wstart) {
+  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < n; r += (uint64_t)gridDim.x * blockDim.x)
+    wstart[r] = wpre[off[r + 1]] - wpre[off[r]];
+}
+
+
+// ---- plan -----------------------------------------------------------------------
+__global__ void k_classify(const uint64_t* __restrict__ wstart, uint64_t n, uint64_t light_max, uint32_t flags,
+                           uint32_t* __restrict__ is_light, uint32_t* __restrict__ is_heavy,
+                           uint32_t* __restrict__ light_w) {
+  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < n; r += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t w = wstart[r];
+    bool light = w > 0 && w <= light_max;
+    bool heavy = w > light_max;
+    if (flags & BF_FLAG_FORCE_WARP) { light = w > 0 && w <= 512; heavy = w > 512; }  // table capacity bound
+    if (flags & BF_FLAG_FORCE_CTA) { heavy = w > 0; light = false; }
+    is_light[r] = light;
+    is_heavy[r] = heavy;
+    light_w[r] = light ? (uint32_t)w : 0u;
+  }
+}
+
+__global__ void k_compact(const uint32_t* __restrict__ flag, const uint32_t* __restrict__ idx, uint64_t n,
+                          uint32_t* __restrict__ out) {
+  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < n; r += (uint64_t)gridDim.x * blockDim.x)
+    if (flag[r]) out[idx[r]] = (uint32_t)r;
+}
+
+__global__ void k_heavy_keys(const uint32_t* __restrict__ heavy, uint32_t nh, const uint64_t* __restrict__ wstart,
+                             uint32_t* __restrict__ key) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nh; i += gridDim.x * blockDim.x) {
+    uint64_t w = wstart[heavy[i]];
+    key[i] = ~(uint32_t)(w > 0xFFFFFFFFull ? 0xFFFFFFFFull : w);  // descending wedges
+  }
+}
+
+__global__ void k_gather_u32_to_u64(const uint32_t* __restrict__ list, uint32_t cnt, const uint64_t* __restrict__ w,
+                                    uint32_t* __restrict__ lw) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x)
+    lw[i] = (uint32_t)w[list[i]];
+}
+
+}  // namespace
+
+bf_status graph_ingest(bf_graph* g, const uint32_t* edges) {
+  cudaStream_t s = g->stream;
+  uint64_t m = g->m, n = g->n;
+  g->edges.ensure(std::max<uint64_t>(m, 1) * 8);
+  g->deg.ensure(std::max<uint64_t>(n, 1) * 4);
+  CUDA_TRY(cudaMemsetAsync(g->deg.p, 0, std::max<uint64_t>(n, 1) * 4, s));
+  if (m) {
+    CUDA_TRY(cudaMemcpyAsync(g->edges.p, edges, m * 8,
+                             g->opt.edges_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+  }
+  g->tmp_a.ensure(64);
+  uint32_t* flags = g->tmp_a.as<uint32_t>();
+  CUDA_TRY(cudaMemsetAsync(flags, 0, 4, s));
+  if (m) {
+    k_validate_degree<<<grid_for(m, g->sms), TPB, 0, s>>>(g->edges.as<uint32_t>(), m, g->n_u, g->n_v,
+                                                          g->deg.as<uint32_t>(), flags);
+    KERNEL_CHECK(g);
+    uint64_t cap = 1;
+    while (cap < 2 * m) cap <<= 1;
+    g->tmp_b.ensure(cap * 8);
+    CUDA_TRY(cudaMemsetAsync(g->tmp_b.p, 0, cap * 8, s));
+    k_dup_check<<<grid_for(m, g->sms), TPB, 0, s>>>(g->edges.as<uint32_t>(), m, g->n_v,
+                                                    g->tmp_b.as<unsigned long long>(), cap - 1, flags);
+    KERNEL_CHECK(g);
+  }
+  uint32_t hflags = 0;
+  CUDA_TRY(cudaMemcpyAsync(&hflags, flags, 4, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  if (hflags & 1u) { bf_set_error("edge id out of range"); return BF_ERANGE; }
+  if (hflags & 2u) { bf_set_error("duplicate edge"); return BF_EDUP; }
+  return BF_OK;
+}
+
+bf_status graph_rank(bf_graph* g, int kind) {
+  cudaStream_t s = g->stream;
+  const uint64_t n = g->n, m = g->m, S = 2 * m;
+  const uint64_t n1 = std::max<uint64_t>(n, 1), S1 = std::max<uint64_t>(S, 1);
+  g->rid_of_gid.ensure(n1 * 4);
+  g->gid_of_rid.ensure(n1 * 4);
+  g->rkey.ensure(n1 * 8);
+  g->off.ensure((n1 + 1) * 4);
+  g->hi.ensure(n1 * 4);
+  g->wstart.ensure(n1 * 8);
+  g->nbr.ensure(S1 * 4);
+  g->pos.ensure(S1 * 4);
+  g->slot_u.ensure(std::max<uint64_t>(m, 1) * 4);
+  g->slot_v.ensure(std::max<uint64_t>(m, 1) * 4);
+  // scratch
+  size_t big = std::max<size_t>(S1, n1);
+  g->tmp_a.ensure(big * 8 + 64);            // keys0 (u64)
+  g->tmp_b.ensure(big * 8 + 64);            // keys1 (u64)
+  g->tmp_c.ensure(big * 4 + 64);            // vals0
+  g->tmp_d.ensure(big * 4 + 64);            // vals1
+  g->tmp_e.ensure((S1 + 1) * 8 + 64);       // wpre / misc
+  g->tmp_f.ensure(big * 4 + 64);            // src / misc
+  g->tmp_scan.ensure(std::max(radix_temp_bytes(big), scan_temp_bytes(S1 + 1)) + 1024);
+  void* tmp = g->tmp_scan.p;
+  uint64_t* L = &g->launches;
+
+  // ---- a2: rank keys, vertex sort -----------------------------------------
+  uint32_t* skey0 = g->tmp_c.as<uint32_t>();
+  uint32_t* skey1 = g->tmp_d.as<uint32_t>();
+  uint32_t* val0 = g->tmp_f.as<uint32_t>();
+  uint32_t* val1 = g->gid_of_rid.as<uint32_t>();
+  uint64_t* rkey_gid = g->tmp_e.as<uint64_t>();
+  unsigned long long* sums = (unsigned long long*)(g->tmp_a.as<char>() + big * 8);  // 16 bytes past keys0
+  CUDA_TRY(cudaMemsetAsync(sums, 0, 16, s));
+  if (n) {
+    k_side_sums<<<grid_for(n, g->sms), TPB, 0, s>>>(g->deg.as<uint32_t>(), n, g->n_u, sums);
+    KERNEL_CHECK(g);
+    k_rank_keys<<<grid_for(n, g->sms), TPB, 0, s>>>(g->deg.as<uint32_t>(), n, g->n_u, kind, sums, skey0, val0,
+                                                     rkey_gid);
+    KERNEL_CHECK(g);
+  }
+  int which = radix_sort_u32(skey0, val0, skey1, val1, n, 0, 32, tmp, s, L);
+  uint32_t* gid_of_rid = which ? val1 : val0;
+  if (gid_of_rid != g->gid_of_rid.as<uint32_t>() && n)
+    CUDA_TRY(cudaMemcpyAsync(g->gid_of_rid.p, gid_of_rid, n * 4, cudaMemcpyDeviceToDevice, s));
+  uint32_t* deg_rid = g->tmp_c.as<uint32_t>();  // skeys no longer needed
+  if (n) {
+    k_rid_maps<<<grid_for(n, g->sms), TPB, 0, s>>>(g->gid_of_rid.as<uint32_t>(), n, g->deg.as<uint32_t>(), rkey_gid,
+                                                    g->rid_of_gid.as<uint32_t>(), g->rkey.as<uint64_t>(), deg_rid);
+    KERNEL_CHECK(g);
+  }
+  // off = exclusive scan of deg_rid; off[n] = 2m
+  scan_exclusive_u32(deg_rid, g->off.as<uint32_t>(), n, g->off.as<uint32_t>() + n, tmp, s, L);
+
+  // ---- a3: slots sorted by (rid(src) asc, rid(dst) desc) --------------------
+  int B = std::max(1, ceil_log2_u64(n1));
+  uint64_t* k0 = g->tmp_a.as<uint64_t>();
+  uint64_t* k1 = g->tmp_b.as<uint64_t>();
+  uint32_t* v0 = g->tmp_c.as<uint32_t>();
+  uint32_t* v1 = g->tmp_d.as<uint32_t>();
+  CUDA_TRY(cudaMemsetAsync(g->hi.p, 0, n1 * 4, s));
+  if (m) {
+    k_slot_keys<<<grid_for(m, g->sms), TPB, 0, s>>>(g->edges.as<uint32_t>(), m, g->n_u, n, B,
+                                                     g->rid_of_gid.as<uint32_t>(), k0, v0);
+    KERNEL_CHECK(g);
+    int w2 = radix_sort_u64(k0, v0, k1, v1, S, 0, 2 * B, tmp, s, L);
+    uint64_t* ks = w2 ? k1 : k0;
+    uint32_t* vs = w2 ? v1 : v0;
+    uint32_t* src = g->tmp_f.as<uint32_t>();
+    uint32_t* where = w2 ? v0 : v1;  // the free vals buffer
+    k_slot_decode<<<grid_for(S, g->sms), TPB, 0, s>>>(ks, vs, S, n, B, g->nbr.as<uint32_t>(), src, where,
+                                                       g->slot_u.as<uint32_t>(), g->slot_v.as<uint32_t>());
+    KERNEL_CHECK(g);
+    k_pos_hi<<<grid_for(S, g->sms), TPB, 0, s>>>(vs, where, g->nbr.as<uint32_t>(), src, g->off.as<uint32_t>(),
+                                                  g->rkey.as<uint64_t>(), S, g->pos.as<uint32_t>(),
+                                                  g->hi.as<uint32_t>());
+    KERNEL_CHECK(g);
+  }
+  g->rank_kind = kind;
+  return BF_OK;
+}
+
+// a4: per-slot wedge counts -> prefix -> per-start counts, W; classification
+bf_status graph_plan(bf_graph* g) {
+  cudaStream_t s = g->stream;
+  const uint64_t n = g->n, m = g->m, S = 2 * m;
+  const uint64_t n1 = std::max<uint64_t>(n, 1), S1 = std::max<uint64_t>(S, 1);
+  void* tmp = g->tmp_scan.p;
+  uint64_t* L = &g->launches;
+  uint32_t* src = g->tmp_f.as<uint32_t>();  // still holds per-slot src from graph_rank
+  uint32_t* wslot = g->tmp_c.as<uint32_t>();
+  uint64_t* wpre = g->tmp_e.as<uint64_t>();
+  uint64_t* dW = g->tmp_b.as<uint64_t>();
+  if (m) {
+    k_wslot<<<grid_for(S, g->sms), TPB, 0, s>>>(g->nbr.as<uint32_t>(), src, g->pos.as<uint32_t>(),
+                                                 g->off.as<uint32_t>(), g->hi.as<uint32_t>(), S, g->orient, wslot);
+    KERNEL_CHECK(g);
+  }
+  scan_exclusive_u32_u64(wslot, wpre, S, wpre + S, tmp, s, L);
+  if (n) {
+    k_wstart<<<grid_for(n, g->sms), TPB, 0, s>>>(wpre, g->off.as<uint32_t>(), n, g->wstart.as<uint64_t>());
+    KERNEL_CHECK(g);
+  }
+  CUDA_TRY(cudaMemcpyAsync(dW, wpre + S, 8, cudaMemcpyDeviceToDevice, s));
+
+  // classification
+  uint64_t light_max = g->opt.test_light_max_wedges ? g->opt.test_light_max_wedges : g->light_max;
+  if (light_max > 512) light_max = 512;  // warp hash capacity: HMAX/2 distinct keys
+  uint32_t* is_light = g->tmp_c.as<uint32_t>();
+  uint32_t* is_heavy = g->tmp_d.as<uint32_t>();
+  uint32_t* light_w = (uint32_t*)g->tmp_a.p;
+  uint32_t* idx_l = (uint32_t*)g->tmp_a.p + n1 + 16;
+  uint32_t* idx_h = g->tmp_f.as<uint32_t>();  // src no longer needed
+  uint32_t* cnts = (uint32_t*)(g->tmp_b.as<char>() + 64);  // [0]=n_light [1]=n_heavy
+  g->light.ensure(n1 * 4);
+  g->heavy.ensure(n1 * 4);
+  g->light_wpre.ensure((n1 + 1) * 8);
+  if (n) {
+    k_classify<<<grid_for(n, g->sms), TPB, 0, s>>>(g->wstart.as<uint64_t>(), n, light_max, g->opt.test_flags,
+                                                    is_light, is_heavy, light_w);
+    KERNEL_CHECK(g);
+  }
+  scan_exclusive_u32(is_light, idx_l, n, cnts + 0, tmp, s, L);
+  scan_exclusive_u32(is_heavy, idx_h, n, cnts + 1, tmp, s, L);
+  if (n) {
+    k_compact<<<grid_for(n, g->sms), TPB, 0, s>>>(is_light, idx_l, n, g->light.as<uint32_t>());
+    KERNEL_CHECK(g);
+    k_compact<<<grid_for(n, g->sms), TPB, 0, s>>>(is_heavy, idx_h, n, g->heavy.as<uint32_t>());
+    KERNEL_CHECK(g);
+  }
+  uint64_t host[2];
+  uint32_t hc[2];
+  CUDA_TRY(cudaMemcpyAsync(host, dW, 8, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaMemcpyAsync(hc, cnts, 8, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  g->W = host[0];
+  g->n_light = hc[0];
+  g->n_heavy = hc[1];
+  // light prefix (for per-rank splits), heavy sorted by wedges desc (LPT-style queue)
+  if (g->n_light) {
+    uint32_t* lw = g->tmp_c.as<uint32_t>();
+    k_gather_u32_to_u64<<<grid_for(g->n_light, g->sms), TPB, 0, s>>>(g->light.as<uint32_t>(), g->n_light,
+                                                                      g->wstart.as<uint64_t>(), lw);
+    KERNEL_CHECK(g);
+    scan_exclusive_u32_u64(lw, g->light_wpre.as<uint64_t>(), g->n_light, g->light_wpre.as<uint64_t>() + g->n_light,
+                           tmp, s, L);
+  }
+  if (g->n_heavy > 1) {
+    uint32_t* hk0 = g->tmp_c.as<uint32_t>();
+    uint32_t* hk1 = g->tmp_d.as<uint32_t>();
+    uint32_t* hv1 = g->tmp_f.as<uint32_t>();
+    k_heavy_keys<<<grid_for(g->n_heavy, g->sms), TPB, 0, s>>>(g->heavy.as<uint32_t>(), g->n_heavy,
+                                                               g->wstart.as<uint64_t>(), hk0);
+    KERNEL_CHECK(g);
+    int w = radix_sort_u32(hk0, g->heavy.as<uint32_t>(), hk1, hv1, g->n_heavy, 0, 32, tmp, s, L);
+    if (w) CUDA_TRY(cudaMemcpyAsync(g->heavy.p, hv1, (size_t)g->n_heavy * 4, cudaMemcpyDeviceToDevice, s));
+  }
+  return BF_OK;
+}

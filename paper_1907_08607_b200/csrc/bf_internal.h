@@ -1,0 +1,125 @@
+// bf_internal.h -- internal declarations of libbf (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stddef.h>
+#include <string>
+#include "../../include/bf.h"
+
+#define BF_SMS_DEFAULT 148
+
+// ---- error plumbing --------------------------------------------------------
+void bf_set_error(const char* fmt, ...);
+struct bf_cuda_error {
+  cudaError_t err;
+  const char* what;
+  int line;
+};
+#define CUDA_TRY(x)                                                   \
+  do {                                                                \
+    cudaError_t e_ = (x);                                             \
+    if (e_ != cudaSuccess) throw bf_cuda_error{e_, #x, __LINE__};     \
+  } while (0)
+#define KERNEL_CHECK(g) do { (g)->launches++; CUDA_TRY(cudaGetLastError()); } while (0)
+
+// ---- scratch allocation ------------------------------------------------------
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  void ensure(size_t n);  // grow (no copy); throws bf_cuda_error
+  void release();
+  template <class T> T* as() const { return (T*)p; }
+};
+
+// ---- primitives (bf_prims.cu) -------------------------------------------------
+// Exclusive scan out[i] = Σ_{j<i} in[j]; *total (device, nullable) = Σ in.
+// Types: (u32->u32), (u64->u64), (u32->u64).
+size_t scan_temp_bytes(size_t n);
+void scan_exclusive_u32(const uint32_t* in, uint32_t* out, size_t n, uint32_t* total, void* temp,
+                        cudaStream_t s, uint64_t* launches);
+void scan_exclusive_u64(const uint64_t* in, uint64_t* out, size_t n, uint64_t* total, void* temp,
+                        cudaStream_t s, uint64_t* launches);
+void scan_exclusive_u32_u64(const uint32_t* in, uint64_t* out, size_t n, uint64_t* total, void* temp,
+                            cudaStream_t s, uint64_t* launches);
+
+// Stable LSD radix sort by bits [begin_bit, end_bit) of the key, carrying u32
+// values (vals may be null).  Ping-pongs between (k0,v0) and (k1,v1); returns
+// 0 if the result is in (k0,v0), 1 if in (k1,v1).
+size_t radix_temp_bytes(size_t n);
+int radix_sort_u32(uint32_t* k0, uint32_t* v0, uint32_t* k1, uint32_t* v1, size_t n, int begin_bit,
+                   int end_bit, void* temp, cudaStream_t s, uint64_t* launches);
+int radix_sort_u64(uint64_t* k0, uint32_t* v0, uint64_t* k1, uint32_t* v1, size_t n, int begin_bit,
+                   int end_bit, void* temp, cudaStream_t s, uint64_t* launches);
+
+static inline int ceil_log2_u64(uint64_t x) {  // bits needed to hold values < x (x>=1)
+  int b = 0;
+  while (b < 64 && ((x - 1) >> b)) b++;
+  return b;
+}
+
+// ---- graph object -----------------------------------------------------------
+struct bf_graph {
+  bf_options opt;
+  int device = 0;
+  int sms = BF_SMS_DEFAULT;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  bool broken = false;  // after a CUDA/NCCL error
+  uint64_t launches = 0;
+
+  uint32_t n_u = 0, n_v = 0;
+  uint64_t n = 0, m = 0;
+
+  // a1: edges + degrees
+  DevBuf edges;  // uint32 [m][2]
+  DevBuf deg;    // uint32 [n], gid order
+
+  // a2/a3: ranking and ranked CSR (rid space)
+  bool ranked = false;
+  int rank_kind = -1;
+  int orient = BF_ORIENT_HIGH;
+  DevBuf rid_of_gid;  // u32 [n]
+  DevBuf gid_of_rid;  // u32 [n]
+  DevBuf rkey;        // u64 [n]  rank key per rid (cross-side comparisons)
+  DevBuf off;         // u32 [n+1]
+  DevBuf nbr;         // u32 [2m]
+  DevBuf pos;         // u32 [2m]  index of src in N(dst)
+  DevBuf hi;          // u32 [n]   deg_x(x)
+  DevBuf slot_u;      // u32 [m]   slot index of edge e's U-side slot
+  DevBuf slot_v;      // u32 [m]   slot index of edge e's V-side slot
+  DevBuf wstart;      // u64 [n]   wedges per start rid (current orientation)
+  uint64_t W = 0;     // total wedges
+
+  // a4: work plan
+  DevBuf heavy;       // u32 list of CTA-path start rids, sorted by wedges desc
+  DevBuf light;       // u32 list of warp-path start rids (ascending rid)
+  DevBuf light_wpre;  // u64 prefix of wedges over `light` (len+1)
+  uint32_t n_heavy = 0, n_light = 0;
+  uint32_t light_max = 0;
+
+  // a5-a7: counting outputs / scratch
+  DevBuf bv;      // u64 [n] per-vertex (rid space)
+  DevBuf acc;     // u64 [2m] per-slot accumulators (edge mode)
+  DevBuf be;      // u64 [m]
+  DevBuf total;   // u64 [4] device scalars
+  DevBuf orow;    // u32 per-CTA global overflow rows
+  DevBuf otouch;  // u32 per-CTA global touched lists
+  DevBuf queue;   // u32 [4] work-queue counters
+  DevBuf pinned_total;  // host-visible staging (cudaMallocHost)
+
+  // temp for primitives
+  DevBuf tmp_a, tmp_b, tmp_c, tmp_d, tmp_e, tmp_f, tmp_scan;
+
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  float last_kernel_ms = 0, last_call_ms = 0;
+};
+
+// ---- phases -------------------------------------------------------------------
+bf_status graph_ingest(bf_graph* g, const uint32_t* edges);        // bf_build.cu
+bf_status graph_rank(bf_graph* g, int kind);                        // bf_build.cu
+bf_status graph_plan(bf_graph* g);                                  // bf_build.cu
+enum { MODE_TOTAL = 0, MODE_VERTEX = 1, MODE_EDGE = 2 };
+bf_status graph_count(bf_graph* g, int mode, uint64_t* out_a, uint64_t* out_b, uint64_t* total);  // bf_count.cu
+
+// NCCL (bf_nccl.cpp)
+bf_status nccl_allreduce_u64(void* comm, uint64_t* buf, size_t count, cudaStream_t s);

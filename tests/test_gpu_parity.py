@@ -1,0 +1,210 @@
+"""GPU parity: libbf (through the C ABI) vs the CPU oracle, element by element.
+
+Integer results must be bit-exact (north_star).  Sizes: tiny
+fixtures, random small graphs, config 1 in full, shrunken copies of configs
+2-5 (same generators) that span many tiles, both tiers and a ragged tail, and
+every code path forced on (warp-only, CTA-only, small shared window -> global
+overflow rows, multi-rank shares via the virtual world).
+"""
+import json
+import os
+from math import comb
+
+import numpy as np
+import pytest
+
+import bfgen
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+RANKS = ("side", "approx_degree", "degree")
+ORIENTS = ("high", "low")
+
+
+@pytest.fixture(scope="module")
+def bf():
+    from paper_1907_08607_b200 import bf as _bf
+    return _bf
+
+
+def run_all(bf, g, rank, orient, **opts):
+    with bf.ButterflyGraph(g.n_u, g.n_v, g.edges, rank=rank, orient=orient, **opts) as bg:
+        t = bg.total()
+        bu, bv, t2 = bg.vertex()
+        be, t3 = bg.edge()
+        w = bg.wedges()
+    return dict(total=t, b_u=bu, b_v=bv, b_e=be, t2=t2, t3=t3, W=w)
+
+
+def assert_same(got, ref, ctx=""):
+    assert got["total"] == ref["total"] == got["t2"] == got["t3"], ctx
+    assert np.array_equal(got["b_u"], ref["b_u"]), ctx + " b_u"
+    assert np.array_equal(got["b_v"], ref["b_v"]), ctx + " b_v"
+    assert np.array_equal(got["b_e"], ref["b_e"]), ctx + " b_e"
+
+
+def test_fig1(bf):
+    d = json.load(open(os.path.join(GOLDEN, "fig1.json")))
+    e = np.array(d["edges"], np.uint32)
+    g = bfgen.from_pairs(3, 3, e)
+    ref = dict(total=d["total"], b_u=np.array(d["b_u"], np.uint64), b_v=np.array(d["b_v"], np.uint64),
+               b_e=np.array(d["b_e"], np.uint64))
+    Ws = {}
+    for rank in RANKS:
+        for orient in ORIENTS:
+            got = run_all(bf, g, rank, orient)
+            assert_same(got, ref, f"{rank}/{orient}")
+            Ws[(rank, orient)] = got["W"]
+    assert Ws[("degree", "low")] == d["wedges_degree_gid_ties"] == Ws[("degree", "high")]
+    assert Ws[("side", "low")] == d["wedges_side_u_first"]
+
+
+@pytest.mark.parametrize("a,b", [(1, 1), (2, 2), (3, 5), (17, 9), (40, 33)])
+def test_complete_bipartite(bf, a, b):
+    g = bfgen.complete(a, b)
+    for rank in RANKS:
+        for orient in ORIENTS:
+            got = run_all(bf, g, rank, orient)
+            assert got["total"] == comb(a, 2) * comb(b, 2)
+            assert (got["b_u"] == (a - 1) * comb(b, 2)).all()
+            assert (got["b_v"] == (b - 1) * comb(a, 2)).all()
+            assert (got["b_e"] == (a - 1) * (b - 1)).all()
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_random_small(bf, seed):
+    rng = np.random.default_rng(1000 + seed)
+    n_u, n_v = int(rng.integers(1, 80)), int(rng.integers(1, 80))
+    p = [0.02, 0.1, 0.3, 0.6][seed % 4]
+    e = np.argwhere(rng.random((n_u, n_v)) < p).astype(np.uint32)
+    e = e[rng.permutation(len(e))]
+    g = bfgen.from_pairs(n_u, n_v, e)
+    ref = oracle.count(n_u, n_v, e)
+    with oracle.OracleGraph(n_u, n_v, e) as og:
+        for rank in RANKS:
+            W_ref = og.wedges(og.rank(rank))[0]
+            for orient in ORIENTS:
+                got = run_all(bf, g, rank, orient)
+                assert_same(got, ref, f"seed {seed} {rank}/{orient}")
+                assert got["W"] == W_ref
+
+
+@pytest.mark.parametrize("flags", ["warp", "cta", "small_window", "cta+small_window", "light8"])
+@pytest.mark.parametrize("orient", ORIENTS)
+def test_forced_paths(bf, flags, orient):
+    """T3: every start through one tier; tiny windows force the global overflow rows."""
+    g = bfgen.chung_lu(1500, 900, 12000, 2.0, 2.3, seed=5)
+    ref = oracle.count(g.n_u, g.n_v, g.edges)
+    f = 0
+    if "warp" in flags:
+        f |= bf.BF_FLAG_FORCE_WARP
+    if "cta" in flags:
+        f |= bf.BF_FLAG_FORCE_CTA
+    if "small_window" in flags:
+        f |= bf.BF_FLAG_SMALL_WINDOW
+    opts = dict(test_flags=f)
+    if flags == "light8":
+        opts["test_light_max_wedges"] = 8
+    if f & bf.BF_FLAG_FORCE_WARP:
+        # warp path needs every start <= its table size; use a graph whose starts are small
+        g = bfgen.uniform(3000, 2500, 9000, seed=3)
+        ref = oracle.count(g.n_u, g.n_v, g.edges)
+    for rank in ("degree", "side"):
+        got = run_all(bf, g, rank, orient, **opts)
+        assert_same(got, ref, f"{flags} {rank}/{orient}")
+
+
+def test_config1_full(bf):
+    """Config 1 in full (BASELINE.json configs[0]) under side and degree ranking."""
+    g = bfgen.config_graph(1)
+    ref = oracle.count(g.n_u, g.n_v, g.edges)
+    for rank in ("side", "degree", "approx_degree"):
+        for orient in ORIENTS:
+            assert_same(run_all(bf, g, rank, orient), ref, f"c1 {rank}/{orient}")
+
+
+@pytest.mark.parametrize("k,scale", [(2, 0.02), (3, 0.01), (4, 0.01), (5, 0.004)])
+def test_configs_scaled(bf, k, scale):
+    """Shrunken configs 2-5 (same generators, same shape): heavy and light tiers,
+    planted biclique (c3), extreme item skew (c4), hub saturation (c5)."""
+    g = bfgen.config_graph(k, scale)
+    ref = oracle.count(g.n_u, g.n_v, g.edges)
+    rank = bfgen.CONFIGS[k]["ranking"][0]
+    for orient in ORIENTS:
+        assert_same(run_all(bf, g, rank, orient), ref, f"c{k}@{scale} {rank}/{orient}")
+
+
+@pytest.mark.parametrize("V", [2, 3, 8])
+def test_virtual_world(bf, V):
+    """T4 on one GPU: each virtual rank counts its share (snake-dealt heavy starts,
+    equal-wedge light slices) and the shares are summed on device."""
+    g = bfgen.config_graph(2, 0.01)
+    ref = oracle.count(g.n_u, g.n_v, g.edges)
+    for orient in ORIENTS:
+        assert_same(run_all(bf, g, "degree", orient, virtual_world=V), ref, f"V={V} {orient}")
+
+
+def test_edge_cases(bf):
+    cases = [bfgen.from_pairs(0, 0, []), bfgen.from_pairs(5, 0, []), bfgen.from_pairs(0, 7, []),
+             bfgen.from_pairs(4, 4, []), bfgen.complete(1, 50), bfgen.complete(50, 1),
+             bfgen.from_pairs(10, 10, [(i, i) for i in range(10)]),
+             bfgen.from_pairs(100, 100, [(3, 4), (3, 7), (9, 4), (9, 7)])]
+    for g in cases:
+        ref = oracle.count(g.n_u, g.n_v, g.edges)
+        for rank in RANKS:
+            for orient in ORIENTS:
+                assert_same(run_all(bf, g, rank, orient), ref, f"{g.name} {rank}/{orient}")
+
+
+def test_errors(bf):
+    with pytest.raises(bf.BFError) as ei:
+        bf.ButterflyGraph(2, 2, np.array([[0, 2]], np.uint32))
+    assert ei.value.status == bf.BF_ERANGE
+    with pytest.raises(bf.BFError) as ei:
+        bf.ButterflyGraph(3, 3, np.array([[0, 1], [2, 2], [0, 1]], np.uint32))
+    assert ei.value.status == bf.BF_EDUP
+    g = bf.ButterflyGraph(2, 2, np.array([[0, 1]], np.uint32), rank=None)
+    with pytest.raises(bf.BFError) as ei:
+        g.total()
+    assert ei.value.status == bf.BF_ENORANK
+    with pytest.raises(bf.BFError) as ei:
+        bf.bf_rank(g.h, 7)
+    assert ei.value.status == bf.BF_EINVAL
+    g.rank("side")
+    assert g.total() == 0
+    g.close()
+
+
+def test_csr_export(bf):
+    """Alg. 1 invariants on the exported ranked CSR: rid is a permutation grouping
+    U before V; lists strictly decreasing; hi/pos per definition; W equals the
+    oracle's W for each ranking."""
+    g = bfgen.chung_lu(700, 500, 5000, 2.1, 2.1, seed=9)
+    n = g.n_u + g.n_v
+    with oracle.OracleGraph(g.n_u, g.n_v, g.edges) as og:
+        for rank in RANKS:
+            rref = og.rank(rank)
+            W_ref, w_ref = og.wedges(rref)
+            with bf.ButterflyGraph(g.n_u, g.n_v, g.edges, rank=rank, orient="low") as bg:
+                c = bg.export_csr()
+                assert bg.wedges() == W_ref
+            rid = c["rid_of_gid"].astype(np.int64)
+            assert sorted(rid.tolist()) == list(range(n))
+            assert (rid[:g.n_u] < g.n_u).all() and (rid[g.n_u:] >= g.n_u).all()
+            # rid order within a side == oracle rank order within the side
+            for lo, hi in ((0, g.n_u), (g.n_u, n)):
+                assert (np.argsort(rid[lo:hi]) == np.argsort(rref[lo:hi])).all()
+            gid_of = np.empty(n, np.int64)
+            gid_of[rid] = np.arange(n)
+            off, nbr, pos, hi_ = c["off"].astype(np.int64), c["nbr"].astype(np.int64), c["pos"], c["hi"]
+            for x in range(0, n, 37):
+                lst = nbr[off[x]:off[x + 1]]
+                assert (np.diff(lst) < 0).all()
+                rx = rref[gid_of[x]]
+                assert hi_[x] == int((rref[gid_of[lst]] > rx).sum())
+                for i, y in enumerate(lst):
+                    assert nbr[off[y] + pos[off[x] + i]] == x
+            # per-start wedges (LOW orientation = Alg. 2 per x1)
+            assert (c["wstart"][rid] == w_ref).all()
