@@ -1,0 +1,461 @@
+#!/usr/bin/env python
+"""bench.py -- exact butterfly counting throughput on B200 (one JSON line).
+
+Workload (default): BASELINE.json configs[1] = config 2, Chung-Lu 1M x 200K,
+10M edges, gamma 2.1/2.1, seed 2, exact per-vertex counts, exact-degree ranking.
+
+A "step" is one pass of the whole hot path over the graph:
+bf_graph_create (ingest, validate, dedup check, degrees) -> bf_rank (ranking,
+ranked CSR, wedge prefix, plan) -> bf_count_vertex (wedge kernels, finalize,
+centre pass, un-rename, allreduce for N > 1) -> bf_graph_destroy, with the edge
+list already resident in HBM.  value = W / t_step (wedges/s) where W is the
+number of wedges the method processes under the ranking (reading Z10).
+
+  python bench.py [--gpus N --steps K --warmup W] [--config k] [--mode vertex|edge|total]
+  python bench.py --impl reference ...   # the CPU oracle on a bounded sample
+
+For N > 1 it is launched by torch.distributed.run, one rank per GPU.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "wedges/sec and edges/sec, exact per-vertex count, 1/2/4/8 B200; % HBM roofline"
+UNIT = "wedges/s"
+CONFIG_DESC = {
+    1: "c1: uniform 2,000 x 1,500, 20,000 distinct edges, seed 1",
+    2: "c2: Chung-Lu |U|=1M, |V|=200K, 10M distinct edges, gamma 2.1/2.1, seed 2",
+    3: "c3: Chung-Lu 3M x 3M, 100M distinct edges, gamma 2.0/2.5, planted K_{200,300}, seed 3",
+    4: "c4: 20M users (Geometric mean 7) x 30K items (Zipf 1.2), seed 4",
+    5: "c5: Chung-Lu 8M x 3M, 300M distinct edges, gamma 1.9/1.9, seed 5",
+}
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--config", type=int, default=2)
+    p.add_argument("--mode", choices=["vertex", "edge", "total"], default="vertex")
+    p.add_argument("--rank", default=None, help="ranking (default: the config's)")
+    p.add_argument("--orient", default="auto", choices=["auto", "low", "high"])
+    p.add_argument("--cpu-seconds", type=float, default=12.0, help="target wall time of the CPU-oracle sample")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    return p.parse_args()
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi samples during the timed region (B200_PROFILING.md clocks line)."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- CPU oracle
+def oracle_sample(g, W: int, target_s: float, mode: str):
+    """Time the plain CPU oracle (as it stands) on a bounded sample of the
+    workload: the first K vertices of its enumeration side (ids are a random
+    permutation, so a prefix is a uniform sample), split over the host cores
+    as independent single-threaded shards.  Returns the extrapolated full-graph
+    rate in wedges/s (W / estimated full oracle time)."""
+    import multiprocessing as mp
+
+    import oracle
+    og = oracle.OracleGraph(g.n_u, g.n_v, g.edges)
+    X = og.cheap_side()
+    deg_y = np.bincount(g.edges[:, 1 - X], minlength=(g.n_u, g.n_v)[1 - X]).astype(np.int64)
+    cost = np.zeros((g.n_u, g.n_v)[X], np.int64)
+    np.add.at(cost, g.edges[:, X].astype(np.int64), deg_y[g.edges[:, 1 - X]])
+    cost = cost * 2 + 1  # two walks per x (pass over N2(x), then the per-edge/centre walk)
+    total_cost = int(cost.sum())
+    P = max(1, len(os.sched_getaffinity(0)))
+    vert, edge = mode == "vertex", mode == "edge"
+    # calibrate single-thread speed on a short prefix
+    t0 = time.perf_counter()
+    k = 0
+    while time.perf_counter() - t0 < 0.3 and k < len(cost):
+        hi = min(len(cost), k + 64)
+        og.count_range(X, k, hi, vertex=vert, edge=edge)
+        k = hi
+    rate = cost[:k].sum() / max(time.perf_counter() - t0, 1e-6)
+    budget = rate * target_s * P
+    csum = np.cumsum(cost)
+    K = int(np.searchsorted(csum, budget)) + 1
+    K = max(P, min(K, len(cost)))
+    cuts = np.searchsorted(csum[:K], np.linspace(0, csum[K - 1], P + 1)[1:-1]).tolist()
+    bounds = list(zip([0] + cuts, cuts + [K]))
+    ctx = mp.get_context("fork")
+    global _OG, _ARGS
+    _OG, _ARGS = og, (X, vert, edge)
+    t0 = time.perf_counter()
+    with ctx.Pool(P) as pool:
+        cpu = pool.map(_oracle_shard, bounds)
+    wall = time.perf_counter() - t0
+    sample_cost = int(csum[K - 1])
+    est_full = wall * total_cost / sample_cost
+    og.close()
+    return dict(value=W / est_full, unit=UNIT, cores=P, kind="oracle",
+                sample=(f"first {K} of {len(cost)} side-{'UV'[X]} vertices ({100.0 * sample_cost / total_cost:.3f}% "
+                        f"of the oracle's 2*sum(deg^2) steps), {P} single-threaded shards, {wall:.2f} s wall, "
+                        f"{sum(cpu):.2f} s CPU; full run extrapolated to {est_full:.1f} s"),
+                est_full_s=est_full, sample_wall_s=wall)
+
+
+_OG = None
+_ARGS = None
+
+
+def _oracle_shard(b):
+    lo, hi = b
+    X, vert, edge = _ARGS
+    t = time.process_time()
+    _OG.count_range(X, lo, hi, vertex=vert, edge=edge)
+    return time.process_time() - t
+
+
+def algorithmic_bytes(mode: str, W: int, m: int, n: int, P: int) -> int:
+    """SURVEY 8(d) per-unit bytes: W wedges, m forward
+    slots, P distinct endpoint pairs, n vertices."""
+    if mode == "vertex":
+        return 8 * W + 48 * m + 16 * P + 28 * n
+    if mode == "edge":
+        return 28 * W + 52 * m + 12 * n
+    return 4 * W + 16 * m + 12 * n
+
+
+def load_traffic(cfg: int, mode: str, orient: str):
+    """dram bytes per launch of the wedge kernel from the committed ncu --set full summary."""
+    import glob
+    for p in sorted(glob.glob(os.path.join(ROOT, "profiles", "*ncu_full*.json")), reverse=True):
+        try:
+            d = json.load(open(p))
+        except Exception:
+            continue
+        if d.get("config") == cfg and d.get("mode") == mode and d.get("orient") == orient:
+            return d.get("dram_bytes_per_launch"), os.path.relpath(p, ROOT)
+    return None, None
+
+
+# ----------------------------------------------------------------------------- main
+def main():
+    a = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    import bfgen
+    cfgd = bfgen.CONFIGS[a.config]
+    rank_kind = a.rank or cfgd["ranking"][0]
+
+    if a.impl == "reference":
+        if rank != 0:
+            return 0
+        return run_reference(a, rank_kind)
+
+    import torch
+    import torch.distributed as dist
+    from paper_1907_08607_b200 import bf
+
+    g = bfgen.config_graph(a.config)
+    n_u, n_v, m = g.n_u, g.n_v, g.m
+    n = n_u + n_v
+
+    # CPU oracle baseline first (rank 0, N = 1 only), before any CUDA work; its W
+    # comes from the oracle's own ranking + wedge definition
+    cpu_base = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        try:
+            import oracle
+            with oracle.OracleGraph(g.n_u, g.n_v, g.edges) as og:
+                W_orc, _ = og.wedges(og.rank(rank_kind))
+            cpu_base = oracle_sample(g, W_orc, a.cpu_seconds, a.mode)
+            cpu_base.pop("est_full_s", None)
+            cpu_base.pop("sample_wall_s", None)
+        except Exception as ex:  # the baseline is reported, never required
+            cpu_base = {"value": None, "unit": UNIT, "cores": 0, "kind": "oracle", "sample": f"failed: {ex}"}
+
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", local if world > 1 else 0)
+    comm = None
+    if world > 1:
+        uid = [bf.bf_nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = bf.bf_nccl_comm_create(uid[0], rank, world, dev.index)
+
+    stream = torch.cuda.current_stream(dev)
+    orient = bf.ORIENTS[a.orient]
+
+    def opts(host: bool):
+        o = bf.bf_options_default()
+        o.device = dev.index
+        o.stream = stream.cuda_stream
+        o.orient = orient
+        if world > 1:
+            o.nccl_comm = comm
+            o.world_rank = rank
+            o.world_size = world
+        o.edges_on_device = 0 if host else 1
+        o.outputs_on_device = 0 if host else 1
+        return o
+
+    edges_dev = torch.from_numpy(g.edges.view(np.int32)).to(dev)
+    out_u = torch.empty(max(n_u, 1), dtype=torch.int64, device=dev)
+    out_v = torch.empty(max(n_v, 1), dtype=torch.int64, device=dev)
+    out_e = torch.empty(max(m, 1), dtype=torch.int64, device=dev)
+    tot = torch.zeros(1, dtype=torch.int64, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def step(host_bufs=None):
+        h = bf.bf_graph_create(n_u, n_v, edges_dev if host_bufs is None else host_bufs["edges"],
+                               opts(host_bufs is not None))
+        try:
+            bf.bf_rank(h, rank_kind)
+            if host_bufs is None:
+                ou, ov, oe, t = out_u, out_v, out_e, tot
+            else:
+                ou, ov, oe, t = host_bufs["u"], host_bufs["v"], host_bufs["e"], host_bufs["t"]
+            if a.mode == "vertex":
+                bf.bf_count_vertex(h, ou, ov, t)
+            elif a.mode == "edge":
+                bf.bf_count_edge(h, oe, t)
+            else:
+                bf.bf_count_total(h, t)
+            kms, cms, pairs = bf.bf_last_stats(h)
+            return dict(W=bf.bf_wedge_count(h), kernel_ms=kms, count_ms=cms, pairs=pairs,
+                        launches=bf.bf_launch_count(h))
+        finally:
+            bf.bf_graph_destroy(h)
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[dev.index])
+
+    # warm-up
+    info = None
+    for _ in range(max(a.warmup, 0)):
+        info = step()
+    torch.cuda.synchronize(dev)
+    W = info["W"] if info else step()["W"]
+
+    # timed region (device-resident inputs)
+    times, kms, launches, pairs = [], [], 0, []
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev.index) as clk:
+        for _ in range(a.steps):
+            flush.fill_(1)  # L2 flush between timed steps (256 MiB > 126 MB L2)
+            torch.cuda.synchronize(dev)
+            barrier()
+            ev0.record(stream)
+            r = step()
+            ev1.record(stream)
+            torch.cuda.synchronize(dev)
+            times.append(ev0.elapsed_time(ev1))
+            kms.append(r["kernel_ms"])
+            launches += r["launches"]
+            pairs.append(r["pairs"])
+    t_local = float(sum(times))
+    t_kernel_local = float(np.mean(kms)) if kms else 0.0
+    if world > 1:
+        tt = torch.tensor([t_local, t_kernel_local], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_max, t_kernel = float(tt[0]), float(tt[1])
+    else:
+        t_max, t_kernel = t_local, t_kernel_local
+    ms_step = t_max / max(a.steps, 1)
+
+    # end-to-end through the public API with host buffers (pinned), H2D + D2H inside
+    e2e = None
+    if not a.no_e2e:
+        hb = {"edges": torch.from_numpy(g.edges.view(np.int32)).pin_memory().numpy().view(np.uint32),
+              "u": torch.empty(max(n_u, 1), dtype=torch.int64).pin_memory().numpy().view(np.uint64),
+              "v": torch.empty(max(n_v, 1), dtype=torch.int64).pin_memory().numpy().view(np.uint64),
+              "e": torch.empty(max(m, 1), dtype=torch.int64).pin_memory().numpy().view(np.uint64),
+              "t": torch.zeros(1, dtype=torch.int64).pin_memory().numpy().view(np.uint64)}
+        step(hb)
+        et = []
+        for _ in range(a.steps):
+            flush.fill_(1)
+            torch.cuda.synchronize(dev)
+            barrier()
+            ev0.record(stream)
+            step(hb)
+            ev1.record(stream)
+            torch.cuda.synchronize(dev)
+            et.append(ev0.elapsed_time(ev1))
+        te = float(sum(et))
+        if world > 1:
+            tt = torch.tensor([te], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            te = float(tt[0])
+        d2h = {"vertex": 8 * (n_u + n_v) + 8, "edge": 8 * m + 8, "total": 8}[a.mode]
+        e2e = {"value": W * a.steps / (te / 1e3), "unit": UNIT, "h2d_bytes_per_step": 8 * m,
+               "d2h_bytes_per_step": d2h, "ms_per_step": te / a.steps}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+
+    value = W * a.steps / (t_max / 1e3)
+    P = int(np.median(pairs)) if pairs else 0
+    abytes = algorithmic_bytes(a.mode, W, m, n, P)
+    if world > 1:  # rank 0's share (the wedge prefix is split evenly)
+        abytes = algorithmic_bytes(a.mode, W // world, m // world, n // world, P)
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    peak = peaks.get("hbm_gbs")
+    peak_src = "MEASURED_PEAKS.json hbm_gbs (measured copy)"
+    if not peak:
+        peak, peak_src = 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+    achieved = abytes / (t_kernel / 1e3) / 1e9 if t_kernel > 0 else None
+    orient_name = a.orient if a.orient != "auto" else "high"
+    traffic, traffic_src = load_traffic(a.config, a.mode, orient_name)
+    out = {
+        "metric": METRIC,
+        "value": value,
+        "unit": UNIT,
+        "n_gpus": world,
+        "steps": a.steps,
+        "warmup": a.warmup,
+        "ms_per_step": ms_step,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "u32/u64",
+        "data": "synthetic",
+        "config": {
+            "workload": CONFIG_DESC[a.config] + f"; exact {a.mode} counts, {rank_kind} ranking",
+            "config": a.config, "n_u": n_u, "n_v": n_v, "m": m, "W": W, "ranking": rank_kind,
+            "orient": orient_name, "mode": a.mode,
+            "step": "bf_graph_create + bf_rank + bf_count_* + destroy (SURVEY 8(a) a1-a9), edges resident in HBM",
+            "l2": "flushed between timed steps (256 MiB device write)",
+            "parallelism": f"dp{world}: wedge-prefix shares of one replicated ranked CSR, NCCL allreduce of outputs",
+        },
+        "edges_per_s": m * a.steps / (t_max / 1e3),
+        "count_only": {"kernel_ms": t_kernel, "wedges_per_s": W / (t_kernel / 1e3) if t_kernel else None,
+                       "edges_per_s": m / (t_kernel / 1e3) if t_kernel else None,
+                       "note": "wedge kernel alone (CUDA events around its launch on the graph's stream)"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                     "kernel": f"k_count<{orient_name},{a.mode}>",
+                     "algorithmic_bytes": abytes, "P_pairs": P,
+                     "bytes_model": {"vertex": "8W+48m+16P+28n", "edge": "28W+52m+12n",
+                                     "total": "4W+16m+12n"}[a.mode],
+                     "peak_source": peak_src, "traffic_source": traffic_src},
+        "cpu_baseline": cpu_base,
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def run_reference(a, rank_kind):
+    """The reference arm: the CPU oracle as it stands, on the box's host cores,
+    each step a bounded sample of the same workload; W from the oracle's own
+    ranking and wedge-count definition (not from the GPU path)."""
+    import bfgen
+    import oracle
+    g = bfgen.config_graph(a.config)
+    with oracle.OracleGraph(g.n_u, g.n_v, g.edges) as og:
+        W, _ = og.wedges(og.rank(rank_kind))
+    per_step = max(2.0, min(a.cpu_seconds, 150.0 / max(1, a.steps + a.warmup)))
+    vals, fulls, last = [], [], None
+    for i in range(a.warmup + a.steps):
+        r = oracle_sample(g, W, per_step, a.mode)
+        if i >= a.warmup:
+            vals.append(r["value"])
+            fulls.append(r["est_full_s"])
+            last = r
+    value = float(np.median(vals))
+    ms = float(np.median(fulls)) * 1e3
+    out = {
+        "impl": "reference",
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "u64", "data": "synthetic",
+        "config": {"workload": CONFIG_DESC[a.config] + f"; exact {a.mode} counts, {rank_kind} ranking",
+                   "config": a.config, "n_u": g.n_u, "n_v": g.n_v, "m": g.m, "W": W, "ranking": rank_kind,
+                   "mode": a.mode},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": last["cores"], "kind": "oracle",
+                         "sample": last["sample"]},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -67,11 +67,13 @@ typedef enum { BF_RANK_SIDE = 0, BF_RANK_APPROX_DEGREE = 1, BF_RANK_DEGREE = 2 }
 typedef enum { BF_ORIENT_AUTO = 0, BF_ORIENT_LOW = 1, BF_ORIENT_HIGH = 2 } bf_orient;
 
 /* test_flags bits (path forcing for tests; 0 in production) */
-#define BF_FLAG_FORCE_WARP      0x1u  /* every start vertex on the warp-hash path     */
-#define BF_FLAG_FORCE_CTA       0x2u  /* every start vertex on the CTA path            */
+#define BF_FLAG_FORCE_WARP      0x1u  /* warp-hash path for every start it can hold (w <= 512),
+                                         dense-window path for the rest                */
+#define BF_FLAG_FORCE_CTA       0x2u  /* no warp path: CTA hash / dense-window paths   */
 #define BF_FLAG_SMALL_WINDOW    0x4u  /* shrink the CTA's shared-memory key window so
                                          most keys take the global-row path           */
 #define BF_FLAG_CHECK_OVERFLOW  0x8u  /* reserved                                      */
+#define BF_FLAG_FORCE_DENSE     0x10u /* every start vertex on the dense-window CTA path */
 
 typedef struct {
   int device;               /* CUDA ordinal                                           */
@@ -127,12 +129,22 @@ bf_status bf_count_edge(bf_graph* g, uint64_t* out_e, uint64_t* total);
  * Errors: BF_EINVAL, BF_ENORANK. */
 bf_status bf_wedge_count(const bf_graph* g, uint64_t* w);
 
-/* Wall time (ms, CUDA events on the graph's stream) of the last
- * bf_count_*'s counting kernels alone, and of its whole call.  Host outputs. */
-bf_status bf_last_timing(const bf_graph* g, float* kernel_ms, float* call_ms);
+/* Statistics of the last bf_count_* call (host outputs, each nullable):
+ * kernel_ms = CUDA-event time of its wedge kernel(s) alone, call_ms = of the
+ * whole call (both on the graph's stream); pairs = distinct endpoint pairs
+ * (x1,x2) with d >= 1 that were aggregated (summed over ranks' shares on this
+ * process; the "P" of the algorithmic-bytes model). */
+bf_status bf_last_stats(const bf_graph* g, float* kernel_ms, float* call_ms, uint64_t* pairs);
 
 /* Number of libbf kernel launches issued since the graph was created. */
 uint64_t bf_launch_count(const bf_graph* g);
+
+/* Multi-GPU share (host-only, no GPU needed): the q-th start index that rank
+ * `rank` of `world` processes inside a tier segment [t0, t1) of the
+ * wedge-sorted start list ("snake" deal: round q takes t0 + q*world +
+ * (q odd ? world-1-rank : rank)); returns t1 when there is none.  The kernels
+ * use the same function.  Wedge-aware batching across GPUs. */
+uint64_t bf_deal_index(uint64_t q, int rank, int world, uint64_t t0, uint64_t t1);
 
 /* Debug/test export of the ranked CSR (device -> host copies).  Any pointer
  * may be NULL.  rid_of_gid[n]: rank-space id of global id gid (U-side vertices

@@ -27,7 +27,7 @@ BF_RANK_SIDE, BF_RANK_APPROX_DEGREE, BF_RANK_DEGREE = 0, 1, 2
 RANK_KINDS = {"side": BF_RANK_SIDE, "approx_degree": BF_RANK_APPROX_DEGREE, "degree": BF_RANK_DEGREE}
 BF_ORIENT_AUTO, BF_ORIENT_LOW, BF_ORIENT_HIGH = 0, 1, 2
 ORIENTS = {"auto": BF_ORIENT_AUTO, "low": BF_ORIENT_LOW, "high": BF_ORIENT_HIGH}
-BF_FLAG_FORCE_WARP, BF_FLAG_FORCE_CTA, BF_FLAG_SMALL_WINDOW = 0x1, 0x2, 0x4
+BF_FLAG_FORCE_WARP, BF_FLAG_FORCE_CTA, BF_FLAG_SMALL_WINDOW, BF_FLAG_FORCE_DENSE = 0x1, 0x2, 0x4, 0x10
 
 
 class bf_options(ctypes.Structure):
@@ -48,8 +48,10 @@ _sig = {
     "bf_count_vertex": (ctypes.c_int, [_vp, _vp, _vp, _vp]),
     "bf_count_edge": (ctypes.c_int, [_vp, _vp, _vp]),
     "bf_wedge_count": (ctypes.c_int, [_vp, _u64p]),
-    "bf_last_timing": (ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_float)]),
+    "bf_last_stats": (ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_float), _u64p]),
     "bf_launch_count": (ctypes.c_uint64, [_vp]),
+    "bf_deal_index": (ctypes.c_uint64, [ctypes.c_uint64, ctypes.c_int, ctypes.c_int, ctypes.c_uint64,
+                                        ctypes.c_uint64]),
     "bf_export_csr": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "bf_nccl_unique_id": (ctypes.c_int, [_vp]),
     "bf_nccl_comm_create": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_vp)]),
@@ -137,14 +139,19 @@ def bf_wedge_count(g) -> int:
     return int(w.value)
 
 
-def bf_last_timing(g):
-    a, b = ctypes.c_float(0), ctypes.c_float(0)
-    _check(_lib.bf_last_timing(g, ctypes.byref(a), ctypes.byref(b)), "bf_last_timing")
-    return float(a.value), float(b.value)
+def bf_last_stats(g):
+    """(kernel_ms, call_ms, pairs) of the last bf_count_* on g."""
+    a, b, p = ctypes.c_float(0), ctypes.c_float(0), ctypes.c_uint64(0)
+    _check(_lib.bf_last_stats(g, ctypes.byref(a), ctypes.byref(b), ctypes.byref(p)), "bf_last_stats")
+    return float(a.value), float(b.value), int(p.value)
 
 
 def bf_launch_count(g) -> int:
     return int(_lib.bf_launch_count(g))
+
+
+def bf_deal_index(q: int, rank: int, world: int, t0: int, t1: int) -> int:
+    return int(_lib.bf_deal_index(q, rank, world, t0, t1))
 
 
 def bf_export_csr(g, n: int, m: int):

@@ -21,12 +21,12 @@ void bf_set_error(const char* fmt, ...) {
 
 void DevBuf::ensure(size_t n) {
   if (n <= bytes && p) return;
-  if (p) { cudaFree(p); p = nullptr; bytes = 0; }
-  CUDA_TRY(cudaMalloc(&p, n));
+  if (p) { CUDA_TRY(cudaFreeAsync(p, s)); p = nullptr; bytes = 0; }
+  CUDA_TRY(cudaMallocAsync(&p, n, s));
   bytes = n;
 }
 void DevBuf::release() {
-  if (p) cudaFree(p);
+  if (p) cudaFreeAsync(p, s);
   p = nullptr;
   bytes = 0;
 }
@@ -95,12 +95,8 @@ const char* bf_last_error(void) { return g_err; }
 void bf_graph_destroy(bf_graph* g) {
   if (!g) return;
   DeviceGuard dg(g->device);
-  cudaStreamSynchronize(g->stream);
-  DevBuf* bufs[] = {&g->edges, &g->deg, &g->rid_of_gid, &g->gid_of_rid, &g->rkey, &g->off, &g->nbr, &g->pos,
-                    &g->hi, &g->slot_u, &g->slot_v, &g->wstart, &g->heavy, &g->light, &g->light_wpre, &g->bv,
-                    &g->acc, &g->be, &g->total, &g->orow, &g->otouch, &g->queue, &g->tmp_a, &g->tmp_b,
-                    &g->tmp_c, &g->tmp_d, &g->tmp_e, &g->tmp_f, &g->tmp_scan};
-  for (DevBuf* b : bufs) b->release();
+  g->for_each_buf([](DevBuf& b) { b.release(); });
+  if (g->stream) cudaStreamSynchronize(g->stream);
   for (auto& e : g->ev)
     if (e) cudaEventDestroy(e);
   if (g->own_stream && g->stream) cudaStreamDestroy(g->stream);
@@ -131,7 +127,6 @@ bf_status bf_graph_create(uint32_t n_u, uint32_t n_v, const uint32_t* edges, uin
   g->n = (uint64_t)n_u + n_v;
   g->m = m;
   g->orient = o.orient == BF_ORIENT_LOW ? BF_ORIENT_LOW : BF_ORIENT_HIGH;
-  g->light_max = 256;
   DeviceGuard dg(g->device);
   bf_status st = guarded(g, [&]() -> bf_status {
     CUDA_TRY(cudaSetDevice(g->device));
@@ -143,6 +138,13 @@ bf_status bf_graph_create(uint32_t n_u, uint32_t n_v, const uint32_t* edges, uin
       g->own_stream = true;
     }
     for (auto& e : g->ev) CUDA_TRY(cudaEventCreate(&e));
+    // stream-ordered allocations from the device's default pool; keep freed
+    // blocks cached so repeated create/destroy does not return to the driver
+    cudaMemPool_t pool;
+    CUDA_TRY(cudaDeviceGetDefaultMemPool(&pool, g->device));
+    uint64_t keep = UINT64_MAX;
+    CUDA_TRY(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    g->for_each_buf([&](DevBuf& b) { b.s = g->stream; });
     return graph_ingest(g, edges);
   });
   if (st != BF_OK) {
@@ -202,14 +204,20 @@ bf_status bf_wedge_count(const bf_graph* g, uint64_t* w) {
   return BF_OK;
 }
 
-bf_status bf_last_timing(const bf_graph* g, float* kernel_ms, float* call_ms) {
+bf_status bf_last_stats(const bf_graph* g, float* kernel_ms, float* call_ms, uint64_t* pairs) {
   if (!g) return BF_EINVAL;
   if (kernel_ms) *kernel_ms = g->last_kernel_ms;
   if (call_ms) *call_ms = g->last_call_ms;
+  if (pairs) *pairs = g->last_pairs;
   return BF_OK;
 }
 
 uint64_t bf_launch_count(const bf_graph* g) { return g ? g->launches : 0; }
+
+uint64_t bf_deal_index(uint64_t q, int rank, int world, uint64_t t0, uint64_t t1) {
+  if (world < 1 || rank < 0 || rank >= world || t1 < t0) return t1;
+  return bf_deal(q, (uint64_t)rank, (uint64_t)world, t0, t1);
+}
 
 bf_status bf_export_csr(const bf_graph* g, uint32_t* rid_of_gid, uint32_t* off, uint32_t* nbr, uint32_t* pos,
                         uint32_t* hi, uint64_t* wstart) {

@@ -174,39 +174,31 @@ __global__ void k_wstart(const uint64_t* __restrict__ wpre, const uint32_t* __re
 
 
 // ---- plan -----------------------------------------------------------------------
-__global__ void k_classify(const uint64_t* __restrict__ wstart, uint64_t n, uint64_t light_max, uint32_t flags,
-                           uint32_t* __restrict__ is_light, uint32_t* __restrict__ is_heavy,
-                           uint32_t* __restrict__ light_w) {
-  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < n; r += (uint64_t)gridDim.x * blockDim.x) {
-    uint64_t w = wstart[r];
-    bool light = w > 0 && w <= light_max;
-    bool heavy = w > light_max;
-    if (flags & BF_FLAG_FORCE_WARP) { light = w > 0 && w <= 512; heavy = w > 512; }  // table capacity bound
-    if (flags & BF_FLAG_FORCE_CTA) { heavy = w > 0; light = false; }
-    is_light[r] = light;
-    is_heavy[r] = heavy;
-    light_w[r] = light ? (uint32_t)w : 0u;
+__global__ void k_order_keys(const uint64_t* __restrict__ wstart, uint64_t n, uint64_t t1, uint64_t t2,
+                             uint32_t* __restrict__ nz, uint32_t* __restrict__ key, uint32_t* __restrict__ cnts) {
+  for (uint64_t r0 = blockIdx.x * (uint64_t)blockDim.x; r0 < n; r0 += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t r = r0 + threadIdx.x;
+    const uint64_t w = r < n ? wstart[r] : 0;
+    if (r < n) {
+      nz[r] = w > 0;
+      key[r] = ~(uint32_t)(w > 0xFFFFFFFFull ? 0xFFFFFFFFull : w);  // descending wedges
+    }
+    const uint32_t a = __popc(__ballot_sync(0xffffffffu, w > 0));
+    const uint32_t b = __popc(__ballot_sync(0xffffffffu, w > t1));
+    const uint32_t c = __popc(__ballot_sync(0xffffffffu, w > t2));
+    if ((threadIdx.x & 31) == 0) {
+      if (a) atomicAdd(&cnts[0], a);
+      if (b) atomicAdd(&cnts[1], b);
+      if (c) atomicAdd(&cnts[2], c);
+    }
   }
 }
 
-__global__ void k_compact(const uint32_t* __restrict__ flag, const uint32_t* __restrict__ idx, uint64_t n,
-                          uint32_t* __restrict__ out) {
+__global__ void k_compact2(const uint32_t* __restrict__ flag, const uint32_t* __restrict__ idx,
+                           const uint32_t* __restrict__ key, uint64_t n, uint32_t* __restrict__ out_rid,
+                           uint32_t* __restrict__ out_key) {
   for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < n; r += (uint64_t)gridDim.x * blockDim.x)
-    if (flag[r]) out[idx[r]] = (uint32_t)r;
-}
-
-__global__ void k_heavy_keys(const uint32_t* __restrict__ heavy, uint32_t nh, const uint64_t* __restrict__ wstart,
-                             uint32_t* __restrict__ key) {
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nh; i += gridDim.x * blockDim.x) {
-    uint64_t w = wstart[heavy[i]];
-    key[i] = ~(uint32_t)(w > 0xFFFFFFFFull ? 0xFFFFFFFFull : w);  // descending wedges
-  }
-}
-
-__global__ void k_gather_u32_to_u64(const uint32_t* __restrict__ list, uint32_t cnt, const uint64_t* __restrict__ w,
-                                    uint32_t* __restrict__ lw) {
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x)
-    lw[i] = (uint32_t)w[list[i]];
+    if (flag[r]) { out_rid[idx[r]] = (uint32_t)r; out_key[idx[r]] = key[r]; }
 }
 
 }  // namespace
@@ -261,10 +253,10 @@ bf_status graph_rank(bf_graph* g, int kind) {
   // scratch
   size_t big = std::max<size_t>(S1, n1);
   g->tmp_a.ensure(big * 8 + 64);            // keys0 (u64)
-  g->tmp_b.ensure(big * 8 + 64);            // keys1 (u64)
+  g->tmp_b.ensure(big * 8 + 256);           // keys1 (u64) + small counters
   g->tmp_c.ensure(big * 4 + 64);            // vals0
   g->tmp_d.ensure(big * 4 + 64);            // vals1
-  g->tmp_e.ensure((S1 + 1) * 8 + 64);       // wpre / misc
+  g->tmp_e.ensure((std::max<size_t>(S1 + 1, n1) + 2) * 8 + 64);  // rkey_gid [n] / wpre [S+1]
   g->tmp_f.ensure(big * 4 + 64);            // src / misc
   g->tmp_scan.ensure(std::max(radix_temp_bytes(big), scan_temp_bytes(S1 + 1)) + 1024);
   void* tmp = g->tmp_scan.p;
@@ -349,57 +341,45 @@ bf_status graph_plan(bf_graph* g) {
   }
   CUDA_TRY(cudaMemcpyAsync(dW, wpre + S, 8, cudaMemcpyDeviceToDevice, s));
 
-  // classification
-  uint64_t light_max = g->opt.test_light_max_wedges ? g->opt.test_light_max_wedges : g->light_max;
-  if (light_max > 512) light_max = 512;  // warp hash capacity: HMAX/2 distinct keys
-  uint32_t* is_light = g->tmp_c.as<uint32_t>();
-  uint32_t* is_heavy = g->tmp_d.as<uint32_t>();
-  uint32_t* light_w = (uint32_t*)g->tmp_a.p;
-  uint32_t* idx_l = (uint32_t*)g->tmp_a.p + n1 + 16;
-  uint32_t* idx_h = g->tmp_f.as<uint32_t>();  // src no longer needed
-  uint32_t* cnts = (uint32_t*)(g->tmp_b.as<char>() + 64);  // [0]=n_light [1]=n_heavy
-  g->light.ensure(n1 * 4);
-  g->heavy.ensure(n1 * 4);
-  g->light_wpre.ensure((n1 + 1) * 8);
+  // plan: starts with w > 0, sorted by wedges desc (ties by rid), cut into
+  // heavy / medium / light tier segments
+  uint64_t t1 = g->opt.test_light_max_wedges ? g->opt.test_light_max_wedges : 512;
+  if (t1 > 512) t1 = 512;  // warp hash capacity: 1024 slots hold <= 512 keys at load 1/2
+  uint64_t t2 = 2048;      // medium hash capacity: 4096 slots
+  if (g->opt.test_flags & BF_FLAG_FORCE_WARP) { t1 = 512; t2 = 512; }
+  if (g->opt.test_flags & BF_FLAG_FORCE_CTA) t1 = 0;
+  if (g->opt.test_flags & BF_FLAG_FORCE_DENSE) { t1 = 0; t2 = 0; }
+  g->t1 = (uint32_t)t1;
+  g->t2 = (uint32_t)t2;
+  uint32_t* nzf = g->tmp_c.as<uint32_t>();
+  uint32_t* key = g->tmp_d.as<uint32_t>();
+  uint32_t* idx = (uint32_t*)g->tmp_a.p;
+  uint32_t* k0 = (uint32_t*)g->tmp_a.p + n1 + 16;
+  uint32_t* v0 = g->tmp_f.as<uint32_t>();  // src no longer needed
+  uint32_t* k1 = g->tmp_c.as<uint32_t>();  // reused after compaction
+  uint32_t* cnts = (uint32_t*)(g->tmp_b.as<char>() + 64);  // [0]=nz [1]=w>t1 [2]=w>t2
+  g->order.ensure(n1 * 4);
+  CUDA_TRY(cudaMemsetAsync(cnts, 0, 16, s));
   if (n) {
-    k_classify<<<grid_for(n, g->sms), TPB, 0, s>>>(g->wstart.as<uint64_t>(), n, light_max, g->opt.test_flags,
-                                                    is_light, is_heavy, light_w);
+    k_order_keys<<<grid_for(n, g->sms), TPB, 0, s>>>(g->wstart.as<uint64_t>(), n, t1, t2, nzf, key, cnts);
     KERNEL_CHECK(g);
   }
-  scan_exclusive_u32(is_light, idx_l, n, cnts + 0, tmp, s, L);
-  scan_exclusive_u32(is_heavy, idx_h, n, cnts + 1, tmp, s, L);
+  scan_exclusive_u32(nzf, idx, n, nullptr, tmp, s, L);
   if (n) {
-    k_compact<<<grid_for(n, g->sms), TPB, 0, s>>>(is_light, idx_l, n, g->light.as<uint32_t>());
-    KERNEL_CHECK(g);
-    k_compact<<<grid_for(n, g->sms), TPB, 0, s>>>(is_heavy, idx_h, n, g->heavy.as<uint32_t>());
+    k_compact2<<<grid_for(n, g->sms), TPB, 0, s>>>(nzf, idx, key, n, v0, k0);
     KERNEL_CHECK(g);
   }
-  uint64_t host[2];
-  uint32_t hc[2];
-  CUDA_TRY(cudaMemcpyAsync(host, dW, 8, cudaMemcpyDeviceToHost, s));
-  CUDA_TRY(cudaMemcpyAsync(hc, cnts, 8, cudaMemcpyDeviceToHost, s));
+  uint64_t host = 0;
+  uint32_t hc[3];
+  CUDA_TRY(cudaMemcpyAsync(&host, dW, 8, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaMemcpyAsync(hc, cnts, 12, cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaStreamSynchronize(s));
-  g->W = host[0];
-  g->n_light = hc[0];
-  g->n_heavy = hc[1];
-  // light prefix (for per-rank splits), heavy sorted by wedges desc (LPT-style queue)
-  if (g->n_light) {
-    uint32_t* lw = g->tmp_c.as<uint32_t>();
-    k_gather_u32_to_u64<<<grid_for(g->n_light, g->sms), TPB, 0, s>>>(g->light.as<uint32_t>(), g->n_light,
-                                                                      g->wstart.as<uint64_t>(), lw);
-    KERNEL_CHECK(g);
-    scan_exclusive_u32_u64(lw, g->light_wpre.as<uint64_t>(), g->n_light, g->light_wpre.as<uint64_t>() + g->n_light,
-                           tmp, s, L);
-  }
-  if (g->n_heavy > 1) {
-    uint32_t* hk0 = g->tmp_c.as<uint32_t>();
-    uint32_t* hk1 = g->tmp_d.as<uint32_t>();
-    uint32_t* hv1 = g->tmp_f.as<uint32_t>();
-    k_heavy_keys<<<grid_for(g->n_heavy, g->sms), TPB, 0, s>>>(g->heavy.as<uint32_t>(), g->n_heavy,
-                                                               g->wstart.as<uint64_t>(), hk0);
-    KERNEL_CHECK(g);
-    int w = radix_sort_u32(hk0, g->heavy.as<uint32_t>(), hk1, hv1, g->n_heavy, 0, 32, tmp, s, L);
-    if (w) CUDA_TRY(cudaMemcpyAsync(g->heavy.p, hv1, (size_t)g->n_heavy * 4, cudaMemcpyDeviceToDevice, s));
-  }
+  g->W = host;
+  const uint32_t nnz = hc[0];
+  g->n_tier[0] = hc[2];
+  g->n_tier[1] = hc[1] - hc[2];
+  g->n_tier[2] = nnz - hc[1];
+  int w = radix_sort_u32(k0, v0, k1, g->order.as<uint32_t>(), nnz, 0, 32, tmp, s, L);
+  if (!w && nnz) CUDA_TRY(cudaMemcpyAsync(g->order.p, v0, (size_t)nnz * 4, cudaMemcpyDeviceToDevice, s));
   return BF_OK;
 }

@@ -26,6 +26,7 @@ struct bf_cuda_error {
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
+  cudaStream_t s = nullptr;  // stream-ordered allocation (device default pool)
   void ensure(size_t n);  // grow (no copy); throws bf_cuda_error
   void release();
   template <class T> T* as() const { return (T*)p; }
@@ -55,6 +56,18 @@ static inline int ceil_log2_u64(uint64_t x) {  // bits needed to hold values < x
   int b = 0;
   while (b < 64 && ((x - 1) >> b)) b++;
   return b;
+}
+
+// ---- multi-GPU share (snake deal over a wedge-sorted list) -------------------
+// q-th item of rank r (of G) inside [t0, t1): round q takes index
+// t0 + q*G + (q odd ? G-1-r : r).  Returns t1 when rank r has no q-th item.
+// Used by the kernels and exported (bf_deal_index) for host-side tests.
+#ifdef __CUDACC__
+__host__ __device__
+#endif
+static inline uint64_t bf_deal(uint64_t q, uint64_t r, uint64_t G, uint64_t t0, uint64_t t1) {
+  const uint64_t i = t0 + q * G + ((q & 1u) ? (G - 1 - r) : r);
+  return i < t1 ? i : t1;
 }
 
 // ---- graph object -----------------------------------------------------------
@@ -90,12 +103,12 @@ struct bf_graph {
   DevBuf wstart;      // u64 [n]   wedges per start rid (current orientation)
   uint64_t W = 0;     // total wedges
 
-  // a4: work plan
-  DevBuf heavy;       // u32 list of CTA-path start rids, sorted by wedges desc
-  DevBuf light;       // u32 list of warp-path start rids (ascending rid)
-  DevBuf light_wpre;  // u64 prefix of wedges over `light` (len+1)
-  uint32_t n_heavy = 0, n_light = 0;
-  uint32_t light_max = 0;
+  // a4: work plan: starts with w > 0 sorted by wedges (desc, ties by rid);
+  // tiers are consecutive segments: heavy (w > t2), medium (t1 < w <= t2),
+  // light (w <= t1)
+  DevBuf order;         // u32 [n_tier sum]
+  uint32_t n_tier[3] = {0, 0, 0};
+  uint32_t t1 = 512, t2 = 2048;
 
   // a5-a7: counting outputs / scratch
   DevBuf bv;      // u64 [n] per-vertex (rid space)
@@ -105,13 +118,20 @@ struct bf_graph {
   DevBuf orow;    // u32 per-CTA global overflow rows
   DevBuf otouch;  // u32 per-CTA global touched lists
   DevBuf queue;   // u32 [4] work-queue counters
-  DevBuf pinned_total;  // host-visible staging (cudaMallocHost)
 
   // temp for primitives
   DevBuf tmp_a, tmp_b, tmp_c, tmp_d, tmp_e, tmp_f, tmp_scan;
 
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   float last_kernel_ms = 0, last_call_ms = 0;
+  uint64_t last_pairs = 0;  // distinct endpoint pairs (d >= 1) aggregated by the last count
+
+  template <class F> void for_each_buf(F f) {
+    DevBuf* bufs[] = {&edges, &deg, &rid_of_gid, &gid_of_rid, &rkey, &off, &nbr, &pos, &hi, &slot_u, &slot_v,
+                      &wstart, &order, &bv, &acc, &be, &total, &orow, &otouch, &queue,
+                      &tmp_a, &tmp_b, &tmp_c, &tmp_d, &tmp_e, &tmp_f, &tmp_scan};
+    for (DevBuf* b : bufs) f(*b);
+  }
 };
 
 // ---- phases -------------------------------------------------------------------

@@ -91,7 +91,7 @@ def test_random_small(bf, seed):
                 assert got["W"] == W_ref
 
 
-@pytest.mark.parametrize("flags", ["warp", "cta", "small_window", "cta+small_window", "light8"])
+@pytest.mark.parametrize("flags", ["warp", "cta", "dense", "small_window", "dense+small_window", "light8"])
 @pytest.mark.parametrize("orient", ORIENTS)
 def test_forced_paths(bf, flags, orient):
     """T3: every start through one tier; tiny windows force the global overflow rows."""
@@ -102,15 +102,13 @@ def test_forced_paths(bf, flags, orient):
         f |= bf.BF_FLAG_FORCE_WARP
     if "cta" in flags:
         f |= bf.BF_FLAG_FORCE_CTA
+    if "dense" in flags:
+        f |= bf.BF_FLAG_FORCE_DENSE
     if "small_window" in flags:
         f |= bf.BF_FLAG_SMALL_WINDOW
     opts = dict(test_flags=f)
     if flags == "light8":
         opts["test_light_max_wedges"] = 8
-    if f & bf.BF_FLAG_FORCE_WARP:
-        # warp path needs every start <= its table size; use a graph whose starts are small
-        g = bfgen.uniform(3000, 2500, 9000, seed=3)
-        ref = oracle.count(g.n_u, g.n_v, g.edges)
     for rank in ("degree", "side"):
         got = run_all(bf, g, rank, orient, **opts)
         assert_same(got, ref, f"{flags} {rank}/{orient}")
