@@ -116,16 +116,14 @@ __global__ void k_slot_keys(const uint32_t* __restrict__ e, uint64_t m, uint32_t
 
 __global__ void k_slot_decode(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ vals, uint64_t S,
                               uint64_t n, int B, uint32_t* __restrict__ nbr, uint32_t* __restrict__ src,
-                              uint32_t* __restrict__ where, uint32_t* __restrict__ slot_u, uint32_t* __restrict__ slot_v) {
+                              uint32_t* __restrict__ where) {
   uint64_t mask = (B >= 64) ? ~0ull : ((1ull << B) - 1);
   for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < S; j += (uint64_t)gridDim.x * blockDim.x) {
     uint64_t k = keys[j];
     uint32_t v = vals[j];
     nbr[j] = (uint32_t)(n - 1 - (k & mask));
     src[j] = (uint32_t)(k >> B);
-    where[v] = (uint32_t)j;
-    if (v & 1u) slot_v[v >> 1] = (uint32_t)j;
-    else slot_u[v >> 1] = (uint32_t)j;
+    where[v] = (uint32_t)j;  // where[2e] / where[2e+1] = slot of edge e from its U / V end
   }
 }
 
@@ -145,24 +143,41 @@ __global__ void k_pos_hi(const uint32_t* __restrict__ vals, const uint32_t* __re
   }
 }
 
-// per-slot wedge count under the orientation (a4)
+// per-slot wedge segment under the orientation (a4): the segment of N(y) that
+// slot (x -> y) retrieves, as (first index in nbr, length)
 __global__ void k_wslot(const uint32_t* __restrict__ nbr, const uint32_t* __restrict__ src,
                         const uint32_t* __restrict__ pos, const uint32_t* __restrict__ off,
-                        const uint32_t* __restrict__ hi, uint64_t S, int orient, uint32_t* __restrict__ wslot) {
+                        const uint32_t* __restrict__ hi, uint64_t S, int orient, uint32_t* __restrict__ seglo,
+                        uint32_t* __restrict__ seglen) {
   for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < S; j += (uint64_t)gridDim.x * blockDim.x) {
-    uint32_t x = src[j], y = nbr[j];
-    uint32_t w;
+    const uint32_t x = src[j], y = nbr[j];
+    uint32_t lo, len;
     if (orient == BF_ORIENT_LOW) {
       // Alg. 2: slot i < deg_x(x) retrieves N(y)[0 : deg_x(y)), deg_x(y) = pos
-      w = (j - off[x] < hi[x]) ? pos[j] : 0u;
+      lo = off[y];
+      len = (j - off[x] < hi[x]) ? pos[j] : 0u;
     } else {
       // cache-optimised: x is the higher endpoint; y's neighbours ranked below
       // both x and y: N(y)[max(hi[y], pos+1) : deg(y))
-      uint32_t d = off[y + 1] - off[y];
-      uint32_t st = max(hi[y], pos[j] + 1u);
-      w = d > st ? d - st : 0u;
+      const uint32_t oy = off[y], d = off[y + 1] - oy;
+      const uint32_t st = max(hi[y], pos[j] + 1);
+      lo = oy + st;
+      len = d > st ? d - st : 0u;
     }
-    wslot[j] = w;
+    seglo[j] = lo;
+    seglen[j] = len;
+  }
+}
+
+__global__ void k_items(const uint32_t* __restrict__ order, uint32_t cnt, const uint32_t* __restrict__ off,
+                        const uint32_t* __restrict__ hi, const uint64_t* __restrict__ wstart, int orient,
+                        uint4* __restrict__ items) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
+    const uint32_t s = order[i];
+    const uint32_t j0 = off[s];
+    const uint32_t j1 = orient == BF_ORIENT_LOW ? j0 + hi[s] : off[s + 1];
+    const uint64_t w = wstart[s];
+    items[i] = make_uint4(s, j0, j1, (uint32_t)(w > 0xFFFFFFFFull ? 0xFFFFFFFFull : w));
   }
 }
 
@@ -248,8 +263,7 @@ bf_status graph_rank(bf_graph* g, int kind) {
   g->wstart.ensure(n1 * 8);
   g->nbr.ensure(S1 * 4);
   g->pos.ensure(S1 * 4);
-  g->slot_u.ensure(std::max<uint64_t>(m, 1) * 4);
-  g->slot_v.ensure(std::max<uint64_t>(m, 1) * 4);
+  g->where.ensure(S1 * 4);
   // scratch
   size_t big = std::max<size_t>(S1, n1);
   g->tmp_a.ensure(big * 8 + 64);            // keys0 (u64)
@@ -305,9 +319,8 @@ bf_status graph_rank(bf_graph* g, int kind) {
     uint64_t* ks = w2 ? k1 : k0;
     uint32_t* vs = w2 ? v1 : v0;
     uint32_t* src = g->tmp_f.as<uint32_t>();
-    uint32_t* where = w2 ? v0 : v1;  // the free vals buffer
-    k_slot_decode<<<grid_for(S, g->sms), TPB, 0, s>>>(ks, vs, S, n, B, g->nbr.as<uint32_t>(), src, where,
-                                                       g->slot_u.as<uint32_t>(), g->slot_v.as<uint32_t>());
+    uint32_t* where = g->where.as<uint32_t>();
+    k_slot_decode<<<grid_for(S, g->sms), TPB, 0, s>>>(ks, vs, S, n, B, g->nbr.as<uint32_t>(), src, where);
     KERNEL_CHECK(g);
     k_pos_hi<<<grid_for(S, g->sms), TPB, 0, s>>>(vs, where, g->nbr.as<uint32_t>(), src, g->off.as<uint32_t>(),
                                                   g->rkey.as<uint64_t>(), S, g->pos.as<uint32_t>(),
@@ -326,12 +339,15 @@ bf_status graph_plan(bf_graph* g) {
   void* tmp = g->tmp_scan.p;
   uint64_t* L = &g->launches;
   uint32_t* src = g->tmp_f.as<uint32_t>();  // still holds per-slot src from graph_rank
-  uint32_t* wslot = g->tmp_c.as<uint32_t>();
+  g->seglo.ensure(S1 * 4);
+  g->seglen.ensure(S1 * 4);
+  uint32_t* wslot = g->seglen.as<uint32_t>();
   uint64_t* wpre = g->tmp_e.as<uint64_t>();
   uint64_t* dW = g->tmp_b.as<uint64_t>();
   if (m) {
     k_wslot<<<grid_for(S, g->sms), TPB, 0, s>>>(g->nbr.as<uint32_t>(), src, g->pos.as<uint32_t>(),
-                                                 g->off.as<uint32_t>(), g->hi.as<uint32_t>(), S, g->orient, wslot);
+                                                 g->off.as<uint32_t>(), g->hi.as<uint32_t>(), S, g->orient,
+                                                 g->seglo.as<uint32_t>(), wslot);
     KERNEL_CHECK(g);
   }
   scan_exclusive_u32_u64(wslot, wpre, S, wpre + S, tmp, s, L);
@@ -381,5 +397,12 @@ bf_status graph_plan(bf_graph* g) {
   g->n_tier[2] = nnz - hc[1];
   int w = radix_sort_u32(k0, v0, k1, g->order.as<uint32_t>(), nnz, 0, 32, tmp, s, L);
   if (!w && nnz) CUDA_TRY(cudaMemcpyAsync(g->order.p, v0, (size_t)nnz * 4, cudaMemcpyDeviceToDevice, s));
+  g->items.ensure((size_t)std::max<uint32_t>(nnz, 1) * 16);
+  if (nnz) {
+    k_items<<<grid_for(nnz, g->sms), TPB, 0, s>>>(g->order.as<uint32_t>(), nnz, g->off.as<uint32_t>(),
+                                                   g->hi.as<uint32_t>(), g->wstart.as<uint64_t>(), g->orient,
+                                                   g->items.as<uint4>());
+    KERNEL_CHECK(g);
+  }
   return BF_OK;
 }

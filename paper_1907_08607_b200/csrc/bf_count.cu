@@ -69,7 +69,9 @@ struct CountArgs {
   const uint32_t* pos;
   const uint32_t* hi;
   const uint64_t* wstart;
-  const uint32_t* list;   // starts sorted by wedges desc
+  const uint32_t* seglo;  // per-slot segment start in nbr
+  const uint32_t* seglen; // per-slot segment length
+  const uint4* items;     // planned starts {s, j0, j1, w}, sorted by wedges desc
   uint64_t* bv;           // [n+1] per-vertex (rid space)
   uint64_t* acc;          // [2m] per-slot (edge mode)
   uint64_t* total;        // [0] total, [1] distinct pairs
@@ -94,7 +96,7 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
 // wedge-sorted list: round q takes q*G + (q odd ? G-1-r : r)); EMPTY if none
 __device__ __forceinline__ uint32_t dealt(const CountArgs& a, uint32_t q) {
   const uint64_t i = bf_deal(q, (uint64_t)a.rank, (uint64_t)a.world, a.t0, a.t1);
-  return i < a.t1 ? a.list[i] : EMPTY;
+  return i < a.t1 ? (uint32_t)i : EMPTY;
 }
 
 struct StartInfo {
@@ -104,8 +106,10 @@ struct StartInfo {
 };
 
 template <int ORIENT>
-__device__ __forceinline__ StartInfo start_info(const CountArgs& a, uint32_t s) {
+__device__ __forceinline__ StartInfo start_info(const CountArgs& a, uint32_t item) {
+  const uint4 it = __ldg(a.items + item);
   StartInfo t;
+  const uint32_t s = it.x;
   t.s = s;
   const bool isU = s < a.n_u;
   const uint32_t sb = isU ? 0u : a.n_u;
@@ -113,39 +117,26 @@ __device__ __forceinline__ StartInfo start_info(const CountArgs& a, uint32_t s) 
   const uint32_t sl = s - sb;
   t.keyrange = ORIENT == BF_ORIENT_HIGH ? sl : nside - sl - 1u;
   t.kbase = ORIENT == BF_ORIENT_HIGH ? sb : s + 1u;
-  t.j0 = a.off[s];
-  const uint32_t je = a.off[s + 1];
-  t.j1 = ORIENT == BF_ORIENT_HIGH ? je : t.j0 + a.hi[s];
-  t.w = a.wstart[s];
-  t.wide = (je - t.j0) >= (1u << 26);  // d <= deg(s): guards u32 run sums
+  t.j0 = it.y;
+  t.j1 = it.z;
+  t.w = it.w;
+  t.wide = (t.j1 - t.j0) >= (1u << 26);  // d <= #slots walked: guards u32 run sums
   return t;
-}
-
-// segment of slot j = (s -> y)
-template <int ORIENT>
-__device__ __forceinline__ void segment(const CountArgs& a, uint32_t j, uint32_t& y, uint32_t& lo, uint32_t& len) {
-  y = __ldg(a.nbr + j);
-  const uint32_t p = __ldg(a.pos + j);
-  if (ORIENT == BF_ORIENT_LOW) {
-    lo = __ldg(a.off + y);
-    len = p;
-  } else {
-    const uint32_t oy = __ldg(a.off + y), dy = __ldg(a.off + y + 1) - oy;
-    const uint32_t st = max(__ldg(a.hi + y), p + 1u);
-    lo = oy + st;
-    len = dy > st ? dy - st : 0u;
-  }
 }
 
 // Load the 32-slot sub-batch [b, min(b+32, j1)) into the warp: lane o holds the
 // o-th non-empty segment (lo, exclusive prefix); returns the wedge total.
-template <int ORIENT>
+template <bool NEED_Y>
 __device__ __forceinline__ uint32_t sub_load(const CountArgs& a, uint32_t b, uint32_t j1, WarpScratch& ws,
                                              uint32_t& nnz, uint32_t& lo_r, uint32_t& ex_r) {
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t j = b + lane;
   uint32_t y = 0, lo = 0, len = 0;
-  if (j < j1) segment<ORIENT>(a, j, y, lo, len);
+  if (j < j1) {  // precomputed per-slot segment: one coalesced read
+    lo = __ldg(a.seglo + j);
+    len = __ldg(a.seglen + j);
+    if (NEED_Y) y = __ldg(a.nbr + j);
+  }
   const uint32_t nz = __ballot_sync(FULL, len != 0);
   const uint32_t inc = warp_inclusive_scan(len);
   const uint32_t tot = __shfl_sync(FULL, inc, 31);
@@ -233,20 +224,27 @@ __device__ __forceinline__ uint32_t table_size(uint64_t w, uint32_t keyrange, ui
 
 // ------------------------------------------------------- generic walk passes
 // pass 1 over this warp's sub-batches of one start
+constexpr int UNR = 4;  // 32-wedge windows in flight per warp (memory-level parallelism)
+
 template <int ORIENT, class Insert>
 __device__ __forceinline__ void walk_pass1(const CountArgs& a, const StartInfo& st, uint32_t wi, uint32_t nw,
                                            WarpScratch& ws, Insert&& ins) {
   const uint32_t lane = threadIdx.x & 31;
   for (uint32_t b = st.j0 + wi * 32; b < st.j1; b += nw * 32) {
     uint32_t nnz, lo_r, ex_r;
-    const uint32_t tot = sub_load<ORIENT>(a, b, st.j1, ws, nnz, lo_r, ex_r);
+    const uint32_t tot = sub_load<false>(a, b, st.j1, ws, nnz, lo_r, ex_r);
     uint32_t cur = FULL;
-    for (uint32_t k0 = 0; k0 < tot; k0 += 32) {
-      uint32_t mask, idx;
-      window(k0, nnz, lo_r, ex_r, cur, mask, idx);
-      const bool act = k0 + lane < tot;
-      const uint32_t x2 = act ? __ldg(a.nbr + idx) : 0u;
-      ins(act, x2);
+    for (uint32_t k0 = 0; k0 < tot; k0 += 32 * UNR) {
+      uint32_t idx[UNR], x2[UNR];
+#pragma unroll
+      for (int u = 0; u < UNR; u++) {
+        uint32_t mask;
+        window(k0 + 32 * u, nnz, lo_r, ex_r, cur, mask, idx[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < UNR; u++) x2[u] = (k0 + 32 * u + lane < tot) ? __ldg(a.nbr + idx[u]) : 0u;
+#pragma unroll
+      for (int u = 0; u < UNR; u++) ins(k0 + 32 * u + lane < tot, x2[u]);
     }
     __syncwarp();
   }
@@ -259,20 +257,26 @@ __device__ __forceinline__ void walk_pass2(const CountArgs& a, const StartInfo& 
   const uint32_t lane = threadIdx.x & 31;
   for (uint32_t b = st.j0 + wi * 32; b < st.j1; b += nw * 32) {
     uint32_t nnz, lo_r, ex_r;
-    const uint32_t tot = sub_load<ORIENT>(a, b, st.j1, ws, nnz, lo_r, ex_r);
+    const uint32_t tot = sub_load<MODE == MODE_VERTEX>(a, b, st.j1, ws, nnz, lo_r, ex_r);
     uint32_t cur = FULL;
-    for (uint32_t k0 = 0; k0 < tot; k0 += 32) {
-      uint32_t mask, idx;
-      const uint32_t o = window(k0, nnz, lo_r, ex_r, cur, mask, idx);
-      const bool act = k0 + lane < tot;
-      uint32_t c = 0;
-      if (act) {
-        c = find(__ldg(a.nbr + idx)) - 1u;
-        if (MODE == MODE_EDGE && c) red_add_u64(a.acc + idx, c);  // edge (y, key)
+    for (uint32_t k0 = 0; k0 < tot; k0 += 32 * UNR) {
+      uint32_t idx[UNR], o[UNR], msk[UNR], key[UNR];
+#pragma unroll
+      for (int u = 0; u < UNR; u++) o[u] = window(k0 + 32 * u, nnz, lo_r, ex_r, cur, msk[u], idx[u]);
+#pragma unroll
+      for (int u = 0; u < UNR; u++) key[u] = (k0 + 32 * u + lane < tot) ? __ldg(a.nbr + idx[u]) : 0u;
+#pragma unroll
+      for (int u = 0; u < UNR; u++) {
+        const bool act = k0 + 32 * u + lane < tot;
+        uint32_t c = 0;
+        if (act) {
+          c = find(key[u]) - 1u;
+          if (MODE == MODE_EDGE && c) red_add_u64(a.acc + idx[u], c);  // edge (y, key)
+        }
+        bool head;
+        const uint64_t rs = run_sum(msk[u], c, st.wide, head);
+        if (head && act && rs) ws.sum[o[u]] += rs;
       }
-      bool head;
-      const uint64_t rs = run_sum(mask, c, st.wide, head);
-      if (head && act && rs) ws.sum[o] += rs;
     }
     __syncwarp();
     if (lane < nnz) {
@@ -284,6 +288,150 @@ __device__ __forceinline__ void walk_pass2(const CountArgs& a, const StartInfo& 
       }
     }
     __syncwarp();
+  }
+}
+
+// ------------------------------------------------ CTA-level walk (NW warps)
+// The whole CTA loads a chunk of 32*NW slots, compacts the non-empty segments
+// and prefix-sums them (one block scan of (flag << 40 | len)); warps then take
+// groups of UNR consecutive 32-wedge windows, strided over the chunk's
+// flattened wedges, so every warp gets work even when the start has few slots.
+template <int NW>
+struct CtaScratch {
+  uint32_t lo[32 * NW], ex[32 * NW + 1], y[32 * NW], slot[32 * NW];
+  unsigned long long sum[32 * NW];
+  unsigned long long wt[32];
+  uint32_t nnz, tot;
+};
+
+template <int NW, bool NEED_Y>
+__device__ __forceinline__ void cta_chunk_load(const CountArgs& a, uint32_t b, uint32_t j1, CtaScratch<NW>& cs) {
+  const uint32_t tid = threadIdx.x;
+  const uint32_t j = b + tid;
+  uint32_t lo = 0, len = 0, y = 0;
+  if (j < j1) {
+    lo = __ldg(a.seglo + j);
+    len = __ldg(a.seglen + j);
+    if (NEED_Y) y = __ldg(a.nbr + j);
+  }
+  const unsigned long long v = ((unsigned long long)(len != 0) << 40) | len;
+  unsigned long long tot;
+  const unsigned long long ex = block_exclusive_scan<unsigned long long>(v, cs.wt, &tot);
+  if (len) {
+    const uint32_t o = (uint32_t)(ex >> 40);
+    cs.lo[o] = lo;
+    cs.ex[o] = (uint32_t)(ex & 0xFFFFFFFFFFull);
+    cs.y[o] = y;
+    cs.slot[o] = j;
+    cs.sum[o] = 0;
+  }
+  if (tid == 0) {
+    cs.nnz = (uint32_t)(tot >> 40);
+    cs.tot = (uint32_t)(tot & 0xFFFFFFFFFFull);
+  }
+  __syncthreads();
+}
+
+// ordinal of the segment holding wedge k0 - 1 (FULL for k0 = 0), searching
+// upward from lb with 32-wide ballots
+template <int NW>
+__device__ __forceinline__ uint32_t cta_seek(const CtaScratch<NW>& cs, uint32_t nnz, uint32_t lb, uint32_t k0) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t c = lb + 1 + lane;
+  const bool p = c < nnz && cs.ex[c] < k0;
+  const uint32_t m = __ballot_sync(FULL, p);
+  if (m != FULL) return lb + __popc(m);
+  // more than 32 segments ahead: binary search (ex is increasing)
+  uint32_t lo = lb + 32, hi = nnz;  // ex[lo] < k0 <= ex[hi] (ex[nnz] = +inf)
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (cs.ex[mid] < k0) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+template <int NW>
+__device__ __forceinline__ uint32_t cta_window(const CtaScratch<NW>& cs, uint32_t nnz, uint32_t k0, uint32_t& cur,
+                                               uint32_t& mask, uint32_t& idx) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t c = cur + 1 + lane;
+  uint32_t bit = 0;
+  if (c < nnz) {
+    const uint32_t rel = cs.ex[c] - k0;
+    bit = rel < 32u ? (1u << rel) : 0u;
+  }
+  mask = __reduce_or_sync(FULL, bit);
+  const uint32_t o = cur + __popc(mask & (FULL >> (31 - lane)));
+  idx = cs.lo[o] + (k0 + lane - cs.ex[o]);
+  cur += __popc(mask);
+  return o;
+}
+
+template <int NW, class Insert>
+__device__ __forceinline__ void cta_pass1(const CountArgs& a, const StartInfo& st, CtaScratch<NW>& cs, Insert&& ins) {
+  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (uint32_t b = st.j0; b < st.j1; b += 32 * NW) {
+    cta_chunk_load<NW, false>(a, b, st.j1, cs);
+    const uint32_t nnz = cs.nnz, tot = cs.tot;
+    uint32_t lb = FULL;
+    for (uint32_t K0 = wid * 32 * UNR; K0 < tot; K0 += 32 * UNR * NW) {
+      uint32_t cur = cta_seek(cs, nnz, lb, K0);
+      lb = cur;
+      uint32_t idx[UNR], x2[UNR];
+#pragma unroll
+      for (int u = 0; u < UNR; u++) {
+        uint32_t mask;
+        if (K0 + 32 * u < tot) cta_window(cs, nnz, K0 + 32 * u, cur, mask, idx[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < UNR; u++) x2[u] = (K0 + 32 * u + lane < tot) ? __ldg(a.nbr + idx[u]) : 0u;
+#pragma unroll
+      for (int u = 0; u < UNR; u++) ins(K0 + 32 * u + lane < tot, x2[u]);
+    }
+    __syncthreads();
+  }
+}
+
+template <int NW, int MODE, class Find>
+__device__ __forceinline__ void cta_pass2(const CountArgs& a, const StartInfo& st, CtaScratch<NW>& cs, Find&& find) {
+  const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  for (uint32_t b = st.j0; b < st.j1; b += 32 * NW) {
+    cta_chunk_load<NW, MODE == MODE_VERTEX>(a, b, st.j1, cs);
+    const uint32_t nnz = cs.nnz, tot = cs.tot;
+    uint32_t lb = FULL;
+    for (uint32_t K0 = wid * 32 * UNR; K0 < tot; K0 += 32 * UNR * NW) {
+      uint32_t cur = cta_seek(cs, nnz, lb, K0);
+      lb = cur;
+      uint32_t idx[UNR], o[UNR], msk[UNR], key[UNR];
+#pragma unroll
+      for (int u = 0; u < UNR; u++) {
+        msk[u] = 0; o[u] = 0; idx[u] = 0;
+        if (K0 + 32 * u < tot) o[u] = cta_window(cs, nnz, K0 + 32 * u, cur, msk[u], idx[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < UNR; u++) key[u] = (K0 + 32 * u + lane < tot) ? __ldg(a.nbr + idx[u]) : 0u;
+#pragma unroll
+      for (int u = 0; u < UNR; u++) {
+        const bool act = K0 + 32 * u + lane < tot;
+        uint32_t c = 0;
+        if (act) {
+          c = find(key[u]) - 1u;
+          if (MODE == MODE_EDGE && c) red_add_u64(a.acc + idx[u], c);  // edge (y, key)
+        }
+        bool head;
+        const uint64_t rs = run_sum(msk[u], c, st.wide, head);
+        if (head && act && rs) atomicAdd(&cs.sum[o[u]], (unsigned long long)rs);
+      }
+    }
+    __syncthreads();
+    if (tid < nnz) {
+      const uint64_t v = cs.sum[tid];
+      if (v && !(a.exp & 2)) {
+        if (MODE == MODE_VERTEX) red_add_u64(a.bv + cs.y[tid], v);  // centre y
+        else red_add_u64(a.acc + cs.slot[tid], v);                  // edge (s, y)
+      }
+    }
+    __syncthreads();
   }
 }
 
@@ -314,9 +462,10 @@ __global__ void __launch_bounds__(L_WARPS * 32) k_light(CountArgs a) {
     q0 = __shfl_sync(FULL, q0, 0);
     if (dealt(a, q0) == EMPTY) break;
     for (uint32_t q = q0; q < q0 + L_CHUNK; q++) {
-      const uint32_t s = dealt(a, q);
-      if (s == EMPTY) break;
-      const StartInfo st = start_info<ORIENT>(a, s);
+      const uint32_t it = dealt(a, q);
+      if (it == EMPTY) break;
+      const StartInfo st = start_info<ORIENT>(a, it);
+      const uint32_t s = st.s;
       const uint32_t hs = table_size(st.w, st.keyrange, L_SLOTS);
       const uint32_t hmask = hs - 1, shift = 32 - (31 - __clz(hs));
       for (uint32_t i = lane; i < hs; i += 32) { hk[i] = EMPTY; hv[i] = 0; }
@@ -352,27 +501,25 @@ template <int ORIENT, int MODE>
 __global__ void __launch_bounds__(M_WARPS * 32) k_medium(CountArgs a) {
   __shared__ uint32_t s_hk[M_SLOTS];
   __shared__ uint32_t s_hv[M_SLOTS];
-  __shared__ WarpScratch s_ws[M_WARPS];
+  __shared__ CtaScratch<M_WARPS> cs;
   __shared__ uint32_t s_item;
-  const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const uint32_t tid = threadIdx.x, lane = tid & 31;
   constexpr uint32_t NT = M_WARPS * 32;
-  WarpScratch& ws = s_ws[wid];
-  ws.sum[lane] = 0;
   uint64_t tot_acc = 0, pair_acc = 0;
   for (;;) {
     if (tid == 0) s_item = atomicAdd(a.queue, 1u);
     __syncthreads();
-    const uint32_t s = dealt(a, s_item);
-    if (s == EMPTY) break;
-    const StartInfo st = start_info<ORIENT>(a, s);
+    const uint32_t it = dealt(a, s_item);
+    if (it == EMPTY) break;
+    const StartInfo st = start_info<ORIENT>(a, it);
+    const uint32_t s = st.s;
     const uint32_t hs = table_size(st.w, st.keyrange, M_SLOTS);
     const uint32_t hmask = hs - 1, shift = 32 - (31 - __clz(hs));
     for (uint32_t i = tid; i < hs; i += NT) { s_hk[i] = EMPTY; s_hv[i] = 0; }
     __syncthreads();
-    walk_pass1<ORIENT>(a, st, wid, M_WARPS, ws, [&](bool act, uint32_t key) {
+    cta_pass1<M_WARPS>(a, st, cs, [&](bool act, uint32_t key) {
       if (act) hash_insert(s_hk, s_hv, hmask, shift, key);
     });
-    __syncthreads();
     uint64_t lsum = 0;
     for (uint32_t i = tid; i < hs; i += NT) {
       const uint32_t key = s_hk[i];
@@ -389,27 +536,24 @@ __global__ void __launch_bounds__(M_WARPS * 32) k_medium(CountArgs a) {
       if (lane == 0 && lsum) red_add_u64(a.bv + s, lsum);
     }
     if (MODE != MODE_TOTAL)
-      walk_pass2<ORIENT, MODE>(a, st, wid, M_WARPS, ws,
-                               [&](uint32_t key) { return hash_find(s_hk, s_hv, hmask, shift, key); });
+      cta_pass2<M_WARPS, MODE>(a, st, cs, [&](uint32_t key) { return hash_find(s_hk, s_hv, hmask, shift, key); });
     __syncthreads();
   }
   flush_totals(a, tot_acc, pair_acc);
 }
 
 // ================================================================ heavy tier
-constexpr size_t H_SMEM = (size_t)H_WIN * 4 + (size_t)H_WIN * 2 + sizeof(WarpScratch) * H_WARPS + 64;
+constexpr size_t H_SMEM = (size_t)H_WIN * 4 + (size_t)H_WIN * 2 + sizeof(CtaScratch<H_WARPS>) + 64;
 
 template <int ORIENT, int MODE>
 __global__ void __launch_bounds__(H_WARPS * 32) k_heavy(CountArgs a) {
   extern __shared__ __align__(16) char sm[];
   uint32_t* win = (uint32_t*)sm;
   uint16_t* touch = (uint16_t*)(sm + (size_t)H_WIN * 4);
-  WarpScratch* s_ws = (WarpScratch*)(sm + (size_t)H_WIN * 6);
+  CtaScratch<H_WARPS>& cs = *(CtaScratch<H_WARPS>*)(sm + (size_t)H_WIN * 6);
   __shared__ uint32_t s_item, s_nt, s_no;
-  const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const uint32_t tid = threadIdx.x, lane = tid & 31;
   constexpr uint32_t NT = H_WARPS * 32;
-  WarpScratch& ws = s_ws[wid];
-  ws.sum[lane] = 0;
   for (uint32_t i = tid; i < H_WIN; i += NT) win[i] = 0;
   if (tid == 0) { s_nt = 0; s_no = 0; }
   uint32_t* orow = a.orow + (size_t)blockIdx.x * a.orow_len;
@@ -418,13 +562,14 @@ __global__ void __launch_bounds__(H_WARPS * 32) k_heavy(CountArgs a) {
   for (;;) {
     if (tid == 0) s_item = atomicAdd(a.queue, 1u);
     __syncthreads();
-    const uint32_t s = dealt(a, s_item);
-    if (s == EMPTY) break;
-    const StartInfo st = start_info<ORIENT>(a, s);
+    const uint32_t it = dealt(a, s_item);
+    if (it == EMPTY) break;
+    const StartInfo st = start_info<ORIENT>(a, it);
+    const uint32_t s = st.s;
     const uint32_t wlen = min(a.win, st.keyrange);
     const uint32_t kbase = st.kbase;
     // pass 1: dense window + overflow row, ballot-compacted touched lists
-    walk_pass1<ORIENT>(a, st, wid, H_WARPS, ws, [&](bool act, uint32_t x2) {
+    cta_pass1<H_WARPS>(a, st, cs, [&](bool act, uint32_t x2) {
       const uint32_t key = x2 - kbase;
       bool nw_ = false, no_ = false;
       if (act) {
@@ -473,7 +618,7 @@ __global__ void __launch_bounds__(H_WARPS * 32) k_heavy(CountArgs a) {
     }
     if (MODE != MODE_TOTAL) {
       __syncthreads();
-      walk_pass2<ORIENT, MODE>(a, st, wid, H_WARPS, ws, [&](uint32_t x2) {
+      cta_pass2<H_WARPS, MODE>(a, st, cs, [&](uint32_t x2) {
         const uint32_t key = x2 - kbase;
         return key < wlen ? win[key] : orow[key - wlen];
       });
@@ -497,10 +642,12 @@ __global__ void k_unrename(const uint64_t* __restrict__ bv, const uint32_t* __re
   }
 }
 
-__global__ void k_edge_gather(const uint64_t* __restrict__ acc, const uint32_t* __restrict__ su,
-                              const uint32_t* __restrict__ sv, uint64_t m, uint64_t* __restrict__ be) {
-  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m; e += (uint64_t)gridDim.x * blockDim.x)
-    be[e] = acc[su[e]] + acc[sv[e]];
+__global__ void k_edge_gather(const uint64_t* __restrict__ acc, const uint2* __restrict__ where, uint64_t m,
+                              uint64_t* __restrict__ be) {
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m; e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint2 w = where[e];  // the edge's two slots
+    be[e] = acc[w.x] + acc[w.y];
+  }
 }
 
 inline unsigned grid_for(size_t n, int sms) {
@@ -580,7 +727,9 @@ bf_status graph_count(bf_graph* g, int mode, uint64_t* out_a, uint64_t* out_b, u
   a.pos = g->pos.as<uint32_t>();
   a.hi = g->hi.as<uint32_t>();
   a.wstart = g->wstart.as<uint64_t>();
-  a.list = g->order.as<uint32_t>();
+  a.seglo = g->seglo.as<uint32_t>();
+  a.seglen = g->seglen.as<uint32_t>();
+  a.items = g->items.as<uint4>();
   a.bv = g->bv.as<uint64_t>();
   a.acc = g->acc.as<uint64_t>();
   a.total = dtot;
@@ -623,8 +772,8 @@ bf_status graph_count(bf_graph* g, int mode, uint64_t* out_a, uint64_t* out_b, u
     red_cnt = n + 1;
   } else if (mode == MODE_EDGE) {
     if (m) {
-      k_edge_gather<<<grid_for(m, g->sms), 256, 0, s>>>(g->acc.as<uint64_t>(), g->slot_u.as<uint32_t>(),
-                                                         g->slot_v.as<uint32_t>(), m, g->be.as<uint64_t>());
+      k_edge_gather<<<grid_for(m, g->sms), 256, 0, s>>>(g->acc.as<uint64_t>(), g->where.as<uint2>(), m,
+                                                         g->be.as<uint64_t>());
       KERNEL_CHECK(g);
     }
     CUDA_TRY(cudaMemcpyAsync(g->be.as<uint64_t>() + m, dtot, 8, cudaMemcpyDeviceToDevice, s));

@@ -98,9 +98,11 @@ struct bf_graph {
   DevBuf nbr;         // u32 [2m]
   DevBuf pos;         // u32 [2m]  index of src in N(dst)
   DevBuf hi;          // u32 [n]   deg_x(x)
-  DevBuf slot_u;      // u32 [m]   slot index of edge e's U-side slot
-  DevBuf slot_v;      // u32 [m]   slot index of edge e's V-side slot
+  DevBuf where;       // u32 [2m]  where[2e] / where[2e+1]: slot of input edge e from its U / V end
   DevBuf wstart;      // u64 [n]   wedges per start rid (current orientation)
+  DevBuf seglo;       // u32 [2m]  per slot (s->y): first index in nbr of its wedge segment
+  DevBuf seglen;      // u32 [2m]  per slot: segment length (wedges retrieved through y)
+  DevBuf items;       // uint4 per planned start: {s, j0, j1, min(w, 2^32-1)}
   uint64_t W = 0;     // total wedges
 
   // a4: work plan: starts with w > 0 sorted by wedges (desc, ties by rid);
@@ -127,8 +129,8 @@ struct bf_graph {
   uint64_t last_pairs = 0;  // distinct endpoint pairs (d >= 1) aggregated by the last count
 
   template <class F> void for_each_buf(F f) {
-    DevBuf* bufs[] = {&edges, &deg, &rid_of_gid, &gid_of_rid, &rkey, &off, &nbr, &pos, &hi, &slot_u, &slot_v,
-                      &wstart, &order, &bv, &acc, &be, &total, &orow, &otouch, &queue,
+    DevBuf* bufs[] = {&edges, &deg, &rid_of_gid, &gid_of_rid, &rkey, &off, &nbr, &pos, &hi, &where,
+                      &wstart, &seglo, &seglen, &items, &order, &bv, &acc, &be, &total, &orow, &otouch, &queue,
                       &tmp_a, &tmp_b, &tmp_c, &tmp_d, &tmp_e, &tmp_f, &tmp_scan};
     for (DevBuf* b : bufs) f(*b);
   }
