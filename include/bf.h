@@ -66,14 +66,21 @@ typedef enum { BF_RANK_SIDE = 0, BF_RANK_APPROX_DEGREE = 1, BF_RANK_DEGREE = 2 }
  *  BF_ORIENT_AUTO  library choice (currently HIGH).                          */
 typedef enum { BF_ORIENT_AUTO = 0, BF_ORIENT_LOW = 1, BF_ORIENT_HIGH = 2 } bf_orient;
 
-/* test_flags bits (path forcing for tests; 0 in production) */
-#define BF_FLAG_FORCE_WARP      0x1u  /* warp-hash path for every start it can hold (w <= 512),
-                                         dense-window path for the rest                */
-#define BF_FLAG_FORCE_CTA       0x2u  /* no warp path: CTA hash / dense-window paths   */
-#define BF_FLAG_SMALL_WINDOW    0x4u  /* shrink the CTA's shared-memory key window so
-                                         most keys take the global-row path           */
+/* test_flags bits (path forcing for tests; 0 in production).  Tiers of the
+ * work plan: warp tier (w <= 512 wedges and <= 32 slots; per-warp u16 dense
+ * key window + overflow hash), CTA medium tier (w <= 2048) and CTA heavy tier
+ * (dense shared-memory key window + per-CTA global overflow row).  Results
+ * never depend on these flags. */
+#define BF_FLAG_FORCE_WARP      0x1u  /* no medium tier: warp tier for every start it
+                                         can hold, heavy CTA tier for the rest          */
+#define BF_FLAG_FORCE_CTA       0x2u  /* no warp tier: CTA medium / heavy tiers only    */
+#define BF_FLAG_SMALL_WINDOW    0x4u  /* shrink every shared-memory key window to 64
+                                         keys so most keys take the overflow paths
+                                         (warp hash, CTA global row)                    */
 #define BF_FLAG_CHECK_OVERFLOW  0x8u  /* reserved                                      */
-#define BF_FLAG_FORCE_DENSE     0x10u /* every start vertex on the dense-window CTA path */
+#define BF_FLAG_FORCE_DENSE     0x10u /* every start on the heavy CTA tier             */
+#define BF_FLAG_SMALL_CHUNK     0x20u /* CTA chunks of 64 wedges: every CTA start with
+                                         more wedges takes the multi-chunk path         */
 
 typedef struct {
   int device;               /* CUDA ordinal                                           */

@@ -15,7 +15,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libbf.so")
+# BF_LIB selects another in-tree build (libbf_debug.so: device bounds checks)
+LIB_PATH = os.path.join(_HERE, os.environ.get("BF_LIB", "libbf.so"))
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
@@ -28,6 +29,7 @@ RANK_KINDS = {"side": BF_RANK_SIDE, "approx_degree": BF_RANK_APPROX_DEGREE, "deg
 BF_ORIENT_AUTO, BF_ORIENT_LOW, BF_ORIENT_HIGH = 0, 1, 2
 ORIENTS = {"auto": BF_ORIENT_AUTO, "low": BF_ORIENT_LOW, "high": BF_ORIENT_HIGH}
 BF_FLAG_FORCE_WARP, BF_FLAG_FORCE_CTA, BF_FLAG_SMALL_WINDOW, BF_FLAG_FORCE_DENSE = 0x1, 0x2, 0x4, 0x10
+BF_FLAG_SMALL_CHUNK = 0x20
 
 
 class bf_options(ctypes.Structure):

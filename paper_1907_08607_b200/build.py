@@ -30,16 +30,19 @@ def needs_build() -> bool:
     return any(os.path.getmtime(p) > t for p in deps())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, debug: bool = False) -> str:
+    """debug=True builds libbf_debug.so (device bounds checks, -DBF_DEBUG); load it
+    with BF_LIB=libbf_debug.so."""
+    so = SO.replace("libbf.so", "libbf_debug.so") if debug else SO
+    if not force and not debug and not needs_build():
         return SO
     cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "--shared", "-Xcompiler", "-fPIC", "-Xptxas", "-v" if verbose else "-O3",
-           "-I", os.path.join(HERE, "..", "include"), "-o", SO + ".tmp", *sources(), "-ldl"]
+           *(["-DBF_DEBUG"] if debug else []),
+           "-I", os.path.join(HERE, "..", "include"), "-o", so + ".tmp", *sources(), "-ldl"]
     subprocess.check_call(cmd)
-    os.replace(SO + ".tmp", SO)
-    return SO
+    os.replace(so + ".tmp", so)
+    return so
 
 
 if __name__ == "__main__":
-    build(force=True, verbose="-v" in sys.argv)
-    print(SO)
+    print(build(force=True, verbose="-v" in sys.argv, debug="--debug" in sys.argv))

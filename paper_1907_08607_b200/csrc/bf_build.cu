@@ -189,18 +189,37 @@ __global__ void k_wstart(const uint64_t* __restrict__ wpre, const uint32_t* __re
 
 
 // ---- plan -----------------------------------------------------------------------
-__global__ void k_order_keys(const uint64_t* __restrict__ wstart, uint64_t n, uint64_t t1, uint64_t t2,
+// Tier of a start s (its wedge count w and slot count): 0 = CTA heavy, 1 = CTA
+// medium, 2 = warp.  Sort key: tier, then wedges descending (largest first, an
+// LPT order for the dynamic queues).
+struct TierRule {
+  uint64_t tl, tm;       // warp tier: w <= tl and slots <= ts; medium: w <= tm and slots <= ms
+  uint32_t ts, ms;
+  int no_warp, all_heavy;
+};
+
+__global__ void k_order_keys(const uint64_t* __restrict__ wstart, const uint32_t* __restrict__ off,
+                             const uint32_t* __restrict__ hi, int orient, uint64_t n, TierRule tr,
                              uint32_t* __restrict__ nz, uint32_t* __restrict__ key, uint32_t* __restrict__ cnts) {
   for (uint64_t r0 = blockIdx.x * (uint64_t)blockDim.x; r0 < n; r0 += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t r = r0 + threadIdx.x;
     const uint64_t w = r < n ? wstart[r] : 0;
+    uint32_t tier = 3;
+    if (w > 0) {
+      const uint32_t slots = orient == BF_ORIENT_LOW ? hi[r] : off[r + 1] - off[r];
+      if (tr.all_heavy || w > tr.tm) tier = 0;
+      else if (!tr.no_warp && w <= tr.tl && slots <= tr.ts) tier = 2;
+      else if (slots <= tr.ms) tier = 1;
+      else tier = 0;
+    }
     if (r < n) {
       nz[r] = w > 0;
-      key[r] = ~(uint32_t)(w > 0xFFFFFFFFull ? 0xFFFFFFFFull : w);  // descending wedges
+      const uint32_t wc = (uint32_t)(w > 0x3FFFFFFFull ? 0x3FFFFFFFull : w);
+      key[r] = (tier << 30) | (0x3FFFFFFFu - wc);
     }
     const uint32_t a = __popc(__ballot_sync(0xffffffffu, w > 0));
-    const uint32_t b = __popc(__ballot_sync(0xffffffffu, w > t1));
-    const uint32_t c = __popc(__ballot_sync(0xffffffffu, w > t2));
+    const uint32_t b = __popc(__ballot_sync(0xffffffffu, tier == 0));
+    const uint32_t c = __popc(__ballot_sync(0xffffffffu, tier == 1));
     if ((threadIdx.x & 31) == 0) {
       if (a) atomicAdd(&cnts[0], a);
       if (b) atomicAdd(&cnts[1], b);
@@ -342,7 +361,8 @@ bf_status graph_plan(bf_graph* g) {
   g->seglo.ensure(S1 * 4);
   g->seglen.ensure(S1 * 4);
   uint32_t* wslot = g->seglen.as<uint32_t>();
-  uint64_t* wpre = g->tmp_e.as<uint64_t>();
+  g->wpre.ensure((S1 + 1) * 8);
+  uint64_t* wpre = g->wpre.as<uint64_t>();
   uint64_t* dW = g->tmp_b.as<uint64_t>();
   if (m) {
     k_wslot<<<grid_for(S, g->sms), TPB, 0, s>>>(g->nbr.as<uint32_t>(), src, g->pos.as<uint32_t>(),
@@ -357,27 +377,31 @@ bf_status graph_plan(bf_graph* g) {
   }
   CUDA_TRY(cudaMemcpyAsync(dW, wpre + S, 8, cudaMemcpyDeviceToDevice, s));
 
-  // plan: starts with w > 0, sorted by wedges desc (ties by rid), cut into
-  // heavy / medium / light tier segments
-  uint64_t t1 = g->opt.test_light_max_wedges ? g->opt.test_light_max_wedges : 512;
-  if (t1 > 512) t1 = 512;  // warp hash capacity: 1024 slots hold <= 512 keys at load 1/2
-  uint64_t t2 = 2048;      // medium hash capacity: 4096 slots
-  if (g->opt.test_flags & BF_FLAG_FORCE_WARP) { t1 = 512; t2 = 512; }
-  if (g->opt.test_flags & BF_FLAG_FORCE_CTA) t1 = 0;
-  if (g->opt.test_flags & BF_FLAG_FORCE_DENSE) { t1 = 0; t2 = 0; }
-  g->t1 = (uint32_t)t1;
-  g->t2 = (uint32_t)t2;
+  // plan: starts with w > 0, sorted by (tier, wedges desc); tiers are
+  // consecutive segments: CTA heavy, CTA medium, warp
+  TierRule tr;
+  tr.tl = g->opt.test_light_max_wedges ? std::min<uint64_t>(g->opt.test_light_max_wedges, BF_WARP_MAX_WEDGES)
+                                       : BF_WARP_MAX_WEDGES;
+  tr.tm = BF_MEDIUM_MAX_WEDGES;
+  tr.ts = BF_WARP_MAX_SLOTS;
+  tr.ms = BF_MEDIUM_MAX_SLOTS;
+  tr.no_warp = (g->opt.test_flags & BF_FLAG_FORCE_CTA) != 0;
+  tr.all_heavy = (g->opt.test_flags & BF_FLAG_FORCE_DENSE) != 0;
+  if (g->opt.test_flags & BF_FLAG_FORCE_WARP) tr.tm = tr.tl;
+  g->t1 = (uint32_t)tr.tl;
+  g->t2 = (uint32_t)tr.tm;
   uint32_t* nzf = g->tmp_c.as<uint32_t>();
   uint32_t* key = g->tmp_d.as<uint32_t>();
   uint32_t* idx = (uint32_t*)g->tmp_a.p;
   uint32_t* k0 = (uint32_t*)g->tmp_a.p + n1 + 16;
   uint32_t* v0 = g->tmp_f.as<uint32_t>();  // src no longer needed
   uint32_t* k1 = g->tmp_c.as<uint32_t>();  // reused after compaction
-  uint32_t* cnts = (uint32_t*)(g->tmp_b.as<char>() + 64);  // [0]=nz [1]=w>t1 [2]=w>t2
+  uint32_t* cnts = (uint32_t*)(g->tmp_b.as<char>() + 64);  // [0]=nz [1]=tier 0 [2]=tier 1
   g->order.ensure(n1 * 4);
   CUDA_TRY(cudaMemsetAsync(cnts, 0, 16, s));
   if (n) {
-    k_order_keys<<<grid_for(n, g->sms), TPB, 0, s>>>(g->wstart.as<uint64_t>(), n, t1, t2, nzf, key, cnts);
+    k_order_keys<<<grid_for(n, g->sms), TPB, 0, s>>>(g->wstart.as<uint64_t>(), g->off.as<uint32_t>(),
+                                                      g->hi.as<uint32_t>(), g->orient, n, tr, nzf, key, cnts);
     KERNEL_CHECK(g);
   }
   scan_exclusive_u32(nzf, idx, n, nullptr, tmp, s, L);
@@ -392,9 +416,9 @@ bf_status graph_plan(bf_graph* g) {
   CUDA_TRY(cudaStreamSynchronize(s));
   g->W = host;
   const uint32_t nnz = hc[0];
-  g->n_tier[0] = hc[2];
-  g->n_tier[1] = hc[1] - hc[2];
-  g->n_tier[2] = nnz - hc[1];
+  g->n_tier[0] = hc[1];
+  g->n_tier[1] = hc[2];
+  g->n_tier[2] = nnz - hc[1] - hc[2];
   int w = radix_sort_u32(k0, v0, k1, g->order.as<uint32_t>(), nnz, 0, 32, tmp, s, L);
   if (!w && nnz) CUDA_TRY(cudaMemcpyAsync(g->order.p, v0, (size_t)nnz * 4, cudaMemcpyDeviceToDevice, s));
   g->items.ensure((size_t)std::max<uint32_t>(nnz, 1) * 16);

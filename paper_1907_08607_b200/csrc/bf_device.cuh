@@ -2,6 +2,23 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
+
+// Debug bounds checks (libbf_debug.so, built with -DBF_DEBUG): print and trap.
+#ifdef BF_DEBUG
+#define BF_CHECK(c)                                                                                   \
+  do {                                                                                                \
+    if (!(c)) {                                                                                       \
+      printf("BF_CHECK failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #c, blockIdx.x, \
+             threadIdx.x);                                                                            \
+      __trap();                                                                                       \
+    }                                                                                                 \
+  } while (0)
+#else
+#define BF_CHECK(c) \
+  do {              \
+  } while (0)
+#endif
 
 // Exclusive scan of one value per thread across the block (blockDim.x a
 // multiple of 32, <= 1024).  warp_tot: shared scratch of 32 elements.

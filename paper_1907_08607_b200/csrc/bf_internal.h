@@ -8,6 +8,14 @@
 
 #define BF_SMS_DEFAULT 148
 
+// work-plan tiers (a4): warp tier for w <= BF_WARP_MAX_WEDGES and at most
+// BF_WARP_MAX_SLOTS slots; CTA medium tier for w <= BF_MEDIUM_MAX_WEDGES; CTA
+// heavy tier above.  The kernels' shared-memory layouts are sized from these.
+#define BF_WARP_MAX_WEDGES 512u
+#define BF_WARP_MAX_SLOTS 32u
+#define BF_MEDIUM_MAX_WEDGES 2048u
+#define BF_MEDIUM_MAX_SLOTS 128u
+
 // ---- error plumbing --------------------------------------------------------
 void bf_set_error(const char* fmt, ...);
 struct bf_cuda_error {
@@ -101,7 +109,8 @@ struct bf_graph {
   DevBuf where;       // u32 [2m]  where[2e] / where[2e+1]: slot of input edge e from its U / V end
   DevBuf wstart;      // u64 [n]   wedges per start rid (current orientation)
   DevBuf seglo;       // u32 [2m]  per slot (s->y): first index in nbr of its wedge segment
-  DevBuf seglen;      // u32 [2m]  per slot: segment length (wedges retrieved through y)
+  DevBuf seglen;      // u32 [2m]  per slot: segment length (scratch of the plan)
+  DevBuf wpre;        // u64 [2m+1] exclusive prefix of per-slot wedge counts (chunking inside a start)
   DevBuf items;       // uint4 per planned start: {s, j0, j1, min(w, 2^32-1)}
   uint64_t W = 0;     // total wedges
 
@@ -118,7 +127,7 @@ struct bf_graph {
   DevBuf be;      // u64 [m]
   DevBuf total;   // u64 [4] device scalars
   DevBuf orow;    // u32 per-CTA global overflow rows
-  DevBuf otouch;  // u32 per-CTA global touched lists
+  DevBuf otouch;  // u32 per-CTA global touched lists (multi-chunk starts)
   DevBuf queue;   // u32 [4] work-queue counters
 
   // temp for primitives
@@ -130,7 +139,7 @@ struct bf_graph {
 
   template <class F> void for_each_buf(F f) {
     DevBuf* bufs[] = {&edges, &deg, &rid_of_gid, &gid_of_rid, &rkey, &off, &nbr, &pos, &hi, &where,
-                      &wstart, &seglo, &seglen, &items, &order, &bv, &acc, &be, &total, &orow, &otouch, &queue,
+                      &wstart, &seglo, &seglen, &wpre, &items, &order, &bv, &acc, &be, &total, &orow, &otouch, &queue,
                       &tmp_a, &tmp_b, &tmp_c, &tmp_d, &tmp_e, &tmp_f, &tmp_scan};
     for (DevBuf* b : bufs) f(*b);
   }

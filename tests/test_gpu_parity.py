@@ -91,10 +91,13 @@ def test_random_small(bf, seed):
                 assert got["W"] == W_ref
 
 
-@pytest.mark.parametrize("flags", ["warp", "cta", "dense", "small_window", "dense+small_window", "light8"])
+@pytest.mark.parametrize("flags", ["warp", "cta", "dense", "small_window", "dense+small_window", "light8",
+                                   "small_chunk", "dense+small_chunk", "dense+small_window+small_chunk",
+                                   "cta+small_window"])
 @pytest.mark.parametrize("orient", ORIENTS)
 def test_forced_paths(bf, flags, orient):
-    """T3: every start through one tier; tiny windows force the global overflow rows."""
+    """T3: every start through one tier; tiny windows force the overflow paths
+    (warp/medium hash, heavy global rows); tiny chunks force the multi-chunk walk."""
     g = bfgen.chung_lu(1500, 900, 12000, 2.0, 2.3, seed=5)
     ref = oracle.count(g.n_u, g.n_v, g.edges)
     f = 0
@@ -106,6 +109,8 @@ def test_forced_paths(bf, flags, orient):
         f |= bf.BF_FLAG_FORCE_DENSE
     if "small_window" in flags:
         f |= bf.BF_FLAG_SMALL_WINDOW
+    if "small_chunk" in flags:
+        f |= bf.BF_FLAG_SMALL_CHUNK
     opts = dict(test_flags=f)
     if flags == "light8":
         opts["test_light_max_wedges"] = 8

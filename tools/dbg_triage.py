@@ -1,0 +1,41 @@
+"""Run small cases each in a fresh process (CUDA errors are sticky) and report
+which (graph, mode, flags) combinations fail.  Debug tool for GPU bring-up."""
+import json, subprocess, sys, os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+CHILD = r'''
+import sys, json; sys.path.insert(0, ".")
+import bfgen, numpy as np, oracle
+from paper_1907_08607_b200 import bf
+spec = json.loads(sys.argv[1])
+if spec["g"][0] == "K": g = bfgen.complete(*spec["g"][1:])
+else: g = bfgen.chung_lu(*spec["g"][1:])
+ref = oracle.count(g.n_u, g.n_v, g.edges)
+f = 0
+for name in spec["flags"]: f |= getattr(bf, "BF_FLAG_" + name)
+with bf.ButterflyGraph(g.n_u, g.n_v, g.edges, rank=spec["rank"], orient=spec["orient"], test_flags=f) as bg:
+    if spec["mode"] == "total": ok = bg.total() == ref["total"]
+    elif spec["mode"] == "vertex":
+        bu, bv_, t = bg.vertex(); ok = t == ref["total"] and np.array_equal(bu, ref["b_u"]) and np.array_equal(bv_, ref["b_v"])
+    else:
+        be, t = bg.edge(); ok = t == ref["total"] and np.array_equal(be, ref["b_e"])
+print("RESULT", "ok" if ok else "mismatch")
+'''
+
+def main():
+  cases = []
+  for gspec in (["K", 40, 33], ["K", 17, 9], ["C", 1500, 900, 12000, 2.0, 2.3, 5]):
+      for mode in ("total", "vertex", "edge"):
+          for flags in ([], ["FORCE_WARP"], ["FORCE_CTA"], ["FORCE_DENSE"], ["FORCE_DENSE", "SMALL_CHUNK"]):
+              for orient in ("high", "low"):
+                  cases.append(dict(g=gspec, mode=mode, flags=flags, orient=orient, rank="degree"))
+  for c in cases:
+      r = subprocess.run([sys.executable, "-c", CHILD, json.dumps(c)], capture_output=True, text=True, timeout=120)
+      out = (r.stdout + r.stderr)
+      res = "ok" if "RESULT ok" in out else ("mismatch" if "RESULT mismatch" in out else "ERROR")
+      extra = [l for l in out.splitlines() if "BF_CHECK" in l or "BFError" in l][:2]
+      print(res, json.dumps(c), " | ".join(extra)[:300], flush=True)
+
+
+if __name__ == "__main__":
+    main()
