@@ -54,30 +54,6 @@ namespace {
 
 constexpr uint32_t FULL = 0xffffffffu;
 constexpr uint32_t EMPTY = 0xffffffffu;
-constexpr int UNR = 4;  // 32-wedge windows in flight per warp
-
-// warp tier
-constexpr int WT_WARPS = 4;                       // independent warps per CTA
-constexpr uint32_t WT_WIN = 4096;                 // u16 dense window keys per warp
-constexpr uint32_t WT_HS = 512;                   // overflow hash slots per warp (>= max keys)
-constexpr uint32_t WT_TL = BF_WARP_MAX_WEDGES;    // wedges per warp-tier start
-constexpr uint32_t WT_NWIN = WT_TL / 32;
-constexpr uint32_t WT_CHUNK = 8;                  // starts per queue grab
-static_assert(BF_WARP_MAX_SLOTS == 32, "warp tier: one slot per lane");
-static_assert(WT_NWIN % UNR == 0, "warp tier windows unroll");
-
-// medium tier
-constexpr int MD_NT = 128;
-constexpr uint32_t MD_WIN = 8192;                 // u16 dense window keys
-constexpr uint32_t MD_HS = BF_MEDIUM_MAX_WEDGES;  // overflow hash slots (>= max keys)
-constexpr uint32_t MD_CAP = BF_MEDIUM_MAX_WEDGES;
-static_assert(BF_MEDIUM_MAX_SLOTS == MD_NT, "medium tier: one slot per thread");
-
-// heavy tier
-constexpr int HV_NT = 256;
-constexpr uint32_t HV_WIN = 16384;                // u32 dense window keys
-constexpr uint32_t HV_CAP = 4096;                 // wedges per chunk (cached on chip)
-
 struct CountArgs {
   const uint32_t* nbr;
   const uint64_t* wpre;   // [2m+1] per-slot wedge prefix
@@ -94,6 +70,8 @@ struct CountArgs {
   uint32_t t0, t1;        // this tier's segment of the item list
   uint64_t S, n;          // slots, vertices (bounds checks of the debug build)
   uint32_t dbg_stop;      // debug build: stop each start after this phase (0 = never)
+  uint32_t exp;           // timing experiments (env BF_EXPERIMENT; results are wrong when set):
+                          // 1 = skip endpoint REDs, 2 = skip centre REDs
   uint32_t win;           // dense window keys in use (<= compile-time size)
   uint32_t cap;           // heavy chunk capacity in wedges (<= HV_CAP)
   int rank, world;
@@ -241,185 +219,41 @@ struct HeavyStore {
   }
 };
 
-// ================================================================ warp tier
-struct WarpSmem {
-  uint32_t win[WT_WIN / 2];     // u16 counters
-  uint32_t hk[WT_HS];
-  uint32_t hv[WT_HS];
-  uint32_t list[WT_TL];         // distinct keys of the start (owners)
-  uint32_t cache[WT_TL];        // the start's keys in wedge order (pass 2)
-  uint32_t bits[WT_NWIN];       // segment-start bitmap per window
-  unsigned long long ssum[32];  // pass-2 per-segment sums
-  uint8_t sst[WT_TL];           // segment (= lane) starting at each position
-  uint8_t wseg[WT_NWIN];        // segment holding each window's first wedge
-};
-constexpr size_t WT_SMEM = (size_t)WT_WARPS * sizeof(WarpSmem);
-
-template <int ORIENT, int MODE>
-__global__ void __launch_bounds__(WT_WARPS * 32) k_warp(CountArgs a) {
-  extern __shared__ __align__(16) char sm[];
-  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  WarpSmem& ws = ((WarpSmem*)sm)[wid];
-  const uint32_t le = lanemask_le(), lt = lanemask_lt();
-  SmallStore cs;
-  cs.win = ws.win;
-  cs.hk = ws.hk;
-  cs.hv = ws.hv;
-  cs.wl = min(a.win, WT_WIN);
-  cs.hmask = WT_HS - 1;
-  cs.shift = 32 - 9;
-  static_assert(WT_HS == 512, "hash shift");
-  for (uint32_t i = lane; i < WT_WIN / 2; i += 32) ws.win[i] = 0;
-  for (uint32_t i = lane; i < WT_HS; i += 32) { ws.hk[i] = EMPTY; ws.hv[i] = 0; }
-  if (lane < WT_NWIN) ws.bits[lane] = 0;
-  ws.ssum[lane] = 0;
-  __syncwarp();
-  uint64_t tot_acc = 0, pair_acc = 0;
-  for (;;) {
-    uint32_t q0 = 0;
-    if (lane == 0) q0 = atomicAdd(a.queue, WT_CHUNK);
-    q0 = __shfl_sync(FULL, q0, 0);
-    if (dealt(a, q0) == EMPTY) break;
-    for (uint32_t q = q0; q < q0 + WT_CHUNK; q++) {
-      const uint32_t it = dealt(a, q);
-      if (it == EMPTY) break;
-      const Start st = load_start<ORIENT>(a, it);
-      // lane l <-> slot j0 + l: its segment [A, B) of the start's wedges
-      const uint64_t base = __ldg(a.wpre + st.j0);
-      const uint32_t j = st.j0 + lane;
-      uint32_t A = 0, B = 0, dl = 0, yv = 0;
-      if (j < st.j1) {
-        A = (uint32_t)(__ldg(a.wpre + j) - base);
-        B = (uint32_t)(__ldg(a.wpre + j + 1) - base);
-        dl = __ldg(a.seglo + j) - A;
-        if (MODE == MODE_VERTEX) yv = __ldg(a.nbr + j);
-      }
-      const uint32_t tot = __shfl_sync(FULL, B, st.j1 - st.j0 - 1);
-      BF_CHECK(B >= A && B <= WT_TL);
-      if (B > A) {
-        ws.sst[A] = (uint8_t)lane;
-        atomicOr(ws.bits + (A >> 5), 1u << (A & 31));
-        for (uint32_t k = (A + 31) >> 5; (k << 5) < B; k++) ws.wseg[k] = (uint8_t)lane;
-      }
-      __syncwarp();
-      const uint32_t nwin = (tot + 31) >> 5;
-
-      // ---- pass 1: d(key) += 1 per wedge; owners go to the list
-      uint32_t cnt = 0;
-      bool hashed = false;
-      for (uint32_t k0 = 0; k0 < nwin; k0 += UNR) {
-        uint32_t key[UNR];
-#pragma unroll
-        for (int u = 0; u < UNR; u++) {
-          const uint32_t k = k0 + u, pos = (k << 5) + lane;
-          const uint32_t mb = ws.bits[k] & le;
-          const uint32_t o = mb ? ws.sst[(k << 5) + 31 - __clz(mb)] : ws.wseg[k];
-          const uint32_t idx = __shfl_sync(FULL, dl, o) + pos;
-          BF_CHECK(pos >= tot || (o < 32 && idx < a.S));
-          key[u] = pos < tot ? __ldg(a.nbr + idx) : EMPTY;
-        }
-#pragma unroll
-        for (int u = 0; u < UNR; u++) {
-          const uint32_t pos = ((k0 + u) << 5) + lane;
-          bool own = false, h = false;
-          if (pos < tot) {
-            ws.cache[pos] = key[u];
-            own = cs.add(key[u], key[u] - st.kbase, h);
-          }
-          const uint32_t m = __ballot_sync(FULL, own);
-          if (own) ws.list[cnt + __popc(m & lt)] = key[u];
-          cnt += __popc(m);
-          hashed |= __any_sync(FULL, h);
-        }
-      }
-      __syncwarp();
-
-      // ---- finalize: C(d,2) to the total and both endpoints
-      uint64_t lsum = 0;
-      for (uint32_t i = lane; i < cnt; i += 32) {
-        const uint32_t key = ws.list[i], kk = key - st.kbase;
-        BF_CHECK(key < a.n && i < WT_TL);
-        const uint32_t d = cs.get(key, kk);
-        if (MODE == MODE_TOTAL) cs.zero(kk);
-        const uint64_t c = choose2(d);
-        lsum += c;
-        if (MODE == MODE_VERTEX && c) red_add_u64(a.bv + key, c);
-      }
-      if (lane == 0) pair_acc += cnt;
-      tot_acc += lsum;
-      if (MODE == MODE_VERTEX) {
-        const uint64_t t = warp_sum(lsum);
-        if (lane == 0 && t) red_add_u64(a.bv + st.s, t);
-      }
-
-      // ---- pass 2: d-1 to the centre (vertex) or both wedge edges (edge)
-      if (MODE != MODE_TOTAL) {
-        for (uint32_t k = 0; k < nwin; k++) {
-          const uint32_t pos = (k << 5) + lane;
-          const uint32_t bk = ws.bits[k];
-          uint32_t c = 0;
-          if (pos < tot) {
-            const uint32_t key = ws.cache[pos];
-            c = cs.get(key, key - st.kbase) - 1u;
-          }
-          const uint32_t mb = bk & le;
-          const uint32_t o = mb ? ws.sst[(k << 5) + 31 - __clz(mb)] : ws.wseg[k];
-          if (MODE == MODE_EDGE) {
-            const uint32_t idx = __shfl_sync(FULL, dl, o) + pos;
-            if (c) red_add_u64(a.acc + idx, c);  // edge (y, key)
-          }
-          bool head;
-          const uint32_t rs = (uint32_t)run_sum(bk, c, false, head);  // d <= 512: no wrap
-          if (head && rs) ws.ssum[o] += rs;
-        }
-        __syncwarp();
-        const unsigned long long v = ws.ssum[lane];
-        if (v) {
-          if (MODE == MODE_VERTEX) red_add_u64(a.bv + yv, v);  // centre y
-          else red_add_u64(a.acc + j, v);                      // edge (s, y)
-          ws.ssum[lane] = 0;
-        }
-        for (uint32_t i = lane; i < cnt; i += 32) cs.zero(ws.list[i] - st.kbase);
-      }
-      if (hashed)
-        for (uint32_t i = lane; i < WT_HS; i += 32) { ws.hk[i] = EMPTY; ws.hv[i] = 0; }
-      if (lane < nwin) ws.bits[lane] = 0;
-      __syncwarp();
-    }
-  }
-  flush_totals(a, tot_acc, pair_acc);
-}
-
-// ================================================================ CTA tiers
-template <int NT, uint32_t CAPC>
-struct ChunkSmem {
-  using SegT = typename std::conditional<(NT <= 256), uint8_t, uint16_t>::type;
-  uint32_t cache[CAPC];        // keys in wedge order (single-chunk starts)
-  uint32_t own[CAPC / 32];     // owner bit per wedge (single-chunk starts)
-  uint32_t bits[CAPC / 32];
-  uint32_t dlo[NT];            // per segment: nbr index - chunk position
-  uint32_t slo[NT], shi[NT];   // pass-2 per-segment sums
-  uint16_t wseg[CAPC / 32];
-  SegT sst[CAPC];
-  uint32_t jn, item, cnt;
+// ================================================================ unit walk
+// A chunk of a start's wedge sequence (at most NT slots, at most CAP wedges)
+// is cut into "units": pieces of at most P consecutive wedges of one segment.
+// Units are bucketed by length (full pieces first, then halving lengths) so the
+// G-lane groups of a warp walk units of similar length; each lane of a group
+// reads every G-th key of its unit (P/G independent loads in flight per lane).
+// Pass-2 sums of d-1 stay in registers until one shared atomic per unit.
+template <int NT, int P, uint32_t UCAP>
+struct UnitSmem {
+  static constexpr int NCLS = 1 + (P >= 2) + (P >= 4) + (P >= 8) + (P >= 16) + (P >= 32) + (P >= 64);
+  using SlotT = typename std::conditional<(NT <= 256), uint8_t, uint16_t>::type;
+  uint32_t lo[UCAP];           // first nbr index of the unit
+  uint8_t len[UCAP];           // 1..P
+  SlotT slot[UCAP];            // chunk-local slot (thread) of the unit
+  uint32_t slo[NT], shi[NT];   // pass-2 per-slot sums (u64 as two u32)
+  uint32_t ccount[NCLS], cstart[NCLS];
+  uint32_t jn[2];              // continuation slot of chunk i in jn[i & 1] (FULL = none)
+  uint32_t nunits, item, lcnt;
 };
 
-template <int NT, uint32_t CAPC>
-__device__ __forceinline__ uint32_t seg_of(const ChunkSmem<NT, CAPC>& c, uint32_t k, uint32_t le) {
-  BF_CHECK(k < CAPC / 32);
-  const uint32_t mb = c.bits[k] & le;
-  const uint32_t o = mb ? (uint32_t)c.sst[(k << 5) + 31 - __clz(mb)] : (uint32_t)c.wseg[k];
-  BF_CHECK(o < (uint32_t)NT);
-  return o;
+// length class: 0 = full (len == P); c = log2(P) - floor(log2(len)) otherwise
+template <int P>
+__device__ __forceinline__ uint32_t len_class(uint32_t len) {
+  return len >= (uint32_t)P ? 0u : (uint32_t)(31 - __clz(P)) - (uint32_t)(31 - __clz(len));
 }
 
-// Build the chunk [K0, K1) of the start's wedge sequence from slots
+// Build the units of chunk [K0, K1) of the start's wedges from slots
 // [jc, min(jc+NT, j1)).  Thread t handles slot jc + t; `mine` = it has a
-// segment in the chunk.  Returns K1; c.jn receives the slot that continues
-// past K1 (if any).
-template <int MODE, int NT, uint32_t CAPC>
-__device__ __forceinline__ uint64_t chunk_build(const CountArgs& a, ChunkSmem<NT, CAPC>& c, uint32_t jc,
-                                                uint32_t j1, uint64_t base, uint64_t K0, uint32_t cap, bool& mine,
+// segment in the chunk.  Returns K1; u.jn[par] receives the slot that
+// continues past K1 (if any; the caller resets it after reading, and chunks
+// alternate par so the reset never races the next chunk's write).  Three CTA
+// barriers.
+template <int MODE, int NT, int P, uint32_t UCAP>
+__device__ __forceinline__ uint64_t units_build(const CountArgs& a, UnitSmem<NT, P, UCAP>& u, uint32_t jc, uint32_t j1,
+                                                uint64_t base, uint64_t K0, uint32_t cap, uint32_t par, bool& mine,
                                                 uint32_t& myj, uint32_t& myy) {
   const uint32_t tid = threadIdx.x;
   const uint32_t jlim = (j1 - jc > (uint32_t)NT) ? jc + NT : j1;
@@ -430,336 +264,328 @@ __device__ __forceinline__ uint64_t chunk_build(const CountArgs& a, ChunkSmem<NT
   mine = false;
   myj = j;
   myy = 0;
+  uint32_t lo = 0, L = 0;
   if (j < jlim) {
     const uint64_t A = __ldg(a.wpre + j) - base, B = __ldg(a.wpre + j + 1) - base;
-    if (A <= K1 && K1 < B) c.jn = j;
+    if (A <= K1 && K1 < B) u.jn[par] = j;
     if (A < B && A < K1 && B > K0) {  // non-empty segment overlapping [K0, K1)
       const uint64_t a0 = max(A, K0), b0 = min(B, K1);
-      const uint32_t la = (uint32_t)(a0 - K0), lb = (uint32_t)(b0 - K0);
-      BF_CHECK(la < lb && lb <= CAPC && tid < (uint32_t)NT);
-      c.dlo[tid] = __ldg(a.seglo + j) + (uint32_t)(a0 - A) - la;
-      c.sst[la] = (typename ChunkSmem<NT, CAPC>::SegT)tid;
-      atomicOr(c.bits + (la >> 5), 1u << (la & 31));
-      for (uint32_t k = (la + 31) >> 5; (k << 5) < lb; k++) c.wseg[k] = (uint16_t)tid;
+      L = (uint32_t)(b0 - a0);
+      lo = __ldg(a.seglo + j) + (uint32_t)(a0 - A);
       mine = true;
       if (MODE == MODE_VERTEX) myy = __ldg(a.nbr + j);
-      if (MODE != MODE_TOTAL) { c.slo[tid] = 0; c.shi[tid] = 0; }
+      if (MODE != MODE_TOTAL) { u.slo[tid] = 0; u.shi[tid] = 0; }
     }
   }
+  constexpr uint32_t LP = 31 - __builtin_clz(P);
+  const uint32_t nf = L >> LP, r = L & (P - 1);
+  const uint32_t cr = r ? len_class<P>(r) : 0u;
+  uint32_t bf = 0, br = 0;
+  if (nf) bf = atomicAdd(&u.ccount[0], nf);
+  if (r) br = atomicAdd(&u.ccount[cr], 1u);
+  __syncthreads();
+  if (tid == 0) {
+    uint32_t s = 0;
+#pragma unroll
+    for (int c = 0; c < UnitSmem<NT, P, UCAP>::NCLS; c++) {
+      u.cstart[c] = s;
+      s += u.ccount[c];
+      u.ccount[c] = 0;
+    }
+    u.nunits = s;
+    BF_CHECK(s <= UCAP);
+  }
+  __syncthreads();
+  if (L) {
+    const uint32_t b0 = u.cstart[0] + bf;
+    for (uint32_t f = 0; f < nf; f++) {
+      u.lo[b0 + f] = lo + (f << LP);
+      u.len[b0 + f] = (uint8_t)P;
+      u.slot[b0 + f] = (typename UnitSmem<NT, P, UCAP>::SlotT)tid;
+    }
+    if (r) {
+      const uint32_t ur = u.cstart[cr] + br;
+      u.lo[ur] = lo + (nf << LP);
+      u.len[ur] = (uint8_t)r;
+      u.slot[ur] = (typename UnitSmem<NT, P, UCAP>::SlotT)tid;
+    }
+  }
+  __syncthreads();
   return K1;
 }
 
-// Pass-1 windows of one chunk.  LIST: owners append to the global list;
-// otherwise keys and owner bits are cached on chip.
-template <bool LIST, int NT, uint32_t CAPC, class Store>
-__device__ __forceinline__ void chunk_pass1(const CountArgs& a, ChunkSmem<NT, CAPC>& c, const Store& cs,
-                                            uint32_t kbase, uint32_t tot, uint32_t* olist, bool& hashed) {
-  constexpr uint32_t NW = NT / 32;
-  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const uint32_t le = lanemask_le(), lt = lanemask_lt();
-  const uint32_t nwin = (tot + 31) >> 5;
-  BF_CHECK(tot <= CAPC);
-  for (uint32_t k0 = wid * UNR; k0 < nwin; k0 += NW * UNR) {
-    uint32_t key[UNR];
+// owner of a key (its count went 0 -> 1): append it to the start's list
+// (shared memory up to lcap entries, then the CTA's global list)
+__device__ __forceinline__ void list_push(uint32_t* lcnt, uint32_t* list, uint32_t lcap, uint32_t* olist,
+                                          uint64_t ocap, uint32_t key) {
+  const uint32_t i = atomicAdd(lcnt, 1u);
+  if (i < lcap) list[i] = key;
+  else {
+    BF_CHECK(olist != nullptr && i - lcap < ocap);
+    olist[i - lcap] = key;
+  }
+}
+__device__ __forceinline__ uint32_t list_get(const uint32_t* list, uint32_t lcap, const uint32_t* olist, uint32_t i) {
+  return i < lcap ? list[i] : __ldcg(olist + (i - lcap));
+}
+
+// pass 1 over the chunk's units: d(key) += 1 per wedge
+template <int NT, int P, int G, uint32_t UCAP, class Store>
+__device__ __forceinline__ void units_pass1(const CountArgs& a, UnitSmem<NT, P, UCAP>& u, const Store& cs,
+                                            uint32_t kbase, uint32_t* list, uint32_t lcap, uint32_t* olist,
+                                            bool& hashed) {
+  constexpr int IT = P / G;
+  const uint32_t tid = threadIdx.x, gl = tid & (G - 1);
+  const uint32_t nunits = u.nunits;
+  for (uint32_t x = tid / G; x < nunits; x += NT / G) {
+    const uint32_t lo = u.lo[x], len = u.len[x];
+    uint32_t key[IT];
 #pragma unroll
-    for (int u = 0; u < UNR; u++) {
-      const uint32_t k = k0 + u, pos = (k << 5) + lane;
-      key[u] = EMPTY;
-      if (k < nwin) {
-        const uint32_t o = seg_of(c, k, le);
-        BF_CHECK(pos >= tot || (pos < CAPC && c.dlo[o] + pos < a.S));
-        if (pos < tot) key[u] = __ldg(a.nbr + (c.dlo[o] + pos));
-      }
+    for (int it = 0; it < IT; it++) {
+      const uint32_t i = gl + it * G;
+      BF_CHECK(i >= len || lo + i < a.S);
+      key[it] = i < len ? __ldg(a.nbr + (lo + i)) : EMPTY;
     }
 #pragma unroll
-    for (int u = 0; u < UNR; u++) {
-      const uint32_t k = k0 + u, pos = (k << 5) + lane;
-      if (k >= nwin) break;
-      BF_CHECK(pos >= tot || key[u] < a.n);
-      bool own = false;
-      if (pos < tot) {
-        BF_CHECK(__isShared(&c.cache[pos]));
-        if (!LIST) c.cache[pos] = key[u];
-        own = cs.add(key[u], key[u] - kbase, hashed);
-      }
-      const uint32_t m = __ballot_sync(FULL, own);
-      if (!LIST) {
-        if (lane == 0) c.own[k] = m;
-      } else if (m) {
-        const int ld = __ffs(m) - 1;
-        uint32_t b = 0;
-        if ((int)lane == ld) b = atomicAdd(&c.cnt, (uint32_t)__popc(m));
-        b = __shfl_sync(FULL, b, ld);
-        BF_CHECK(!own || b + __popc(m & lt) < a.orow_len);
-        if (own) olist[b + __popc(m & lt)] = key[u];
+    for (int it = 0; it < IT; it++) {
+      if (key[it] != EMPTY) {
+        BF_CHECK(key[it] < a.n);
+        if (cs.add(key[it], key[it] - kbase, hashed)) list_push(&u.lcnt, list, lcap, olist, a.orow_len, key[it]);
       }
     }
   }
 }
 
-// Pass-2 windows of one chunk: c = d(key) - 1 per wedge, summed per segment;
-// edge mode also adds c to the wedge's (y, key) edge.  CACHED: keys from the
-// chunk cache, and owners (owner bits) finalize C(d,2) on the way.
-template <int MODE, bool CACHED, int NT, uint32_t CAPC, class Store>
-__device__ __forceinline__ void chunk_pass2(const CountArgs& a, ChunkSmem<NT, CAPC>& c, const Store& cs,
-                                            uint32_t kbase, uint32_t tot, bool wide, uint64_t& lsum,
-                                            uint64_t& pairs) {
-  constexpr uint32_t NW = NT / 32;
-  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const uint32_t le = lanemask_le();
-  const uint32_t nwin = (tot + 31) >> 5;
-  for (uint32_t k0 = wid * UNR; k0 < nwin; k0 += NW * UNR) {
-    uint32_t key[UNR], o[UNR];
+// pass 2 over the chunk's units: c = d(key) - 1 per wedge, summed per slot
+// (centre y in vertex mode, edge (s, y) in edge mode); edge mode also adds c
+// to the wedge's (y, key) edge
+template <int MODE, int NT, int P, int G, uint32_t UCAP, class Store>
+__device__ __forceinline__ void units_pass2(const CountArgs& a, UnitSmem<NT, P, UCAP>& u, const Store& cs,
+                                            uint32_t kbase) {
+  constexpr int IT = P / G;
+  const uint32_t tid = threadIdx.x, gl = tid & (G - 1);
+  const uint32_t nunits = u.nunits;
+  // warp-uniform trip count: the group reduction below is a full-warp shuffle
+  for (uint32_t xb = (tid & ~31u) / G; xb < nunits; xb += NT / G) {
+    const uint32_t x = xb + (tid & 31) / G;
+    const bool act = x < nunits;
+    const uint32_t lo = act ? u.lo[x] : 0u, len = act ? u.len[x] : 0u;
+    uint32_t key[IT];
 #pragma unroll
-    for (int u = 0; u < UNR; u++) {
-      const uint32_t k = k0 + u, pos = (k << 5) + lane;
-      key[u] = EMPTY;
-      o[u] = 0;
-      if (k < nwin) {
-        o[u] = seg_of(c, k, le);
-        BF_CHECK(pos >= tot || CACHED || c.dlo[o[u]] + pos < a.S);
-        if (pos < tot) key[u] = CACHED ? c.cache[pos] : __ldg(a.nbr + (c.dlo[o[u]] + pos));
-        BF_CHECK(pos >= tot || key[u] < a.n);
+    for (int it = 0; it < IT; it++) {
+      const uint32_t i = gl + it * G;
+      key[it] = i < len ? __ldg(a.nbr + (lo + i)) : EMPTY;
+    }
+    uint64_t s = 0;
+#pragma unroll
+    for (int it = 0; it < IT; it++) {
+      if (key[it] != EMPTY) {
+        const uint32_t c = cs.get(key[it], key[it] - kbase) - 1u;
+        s += c;
+        if (MODE == MODE_EDGE && c) red_add_u64(a.acc + (lo + gl + it * G), c);  // edge (y, key)
       }
     }
 #pragma unroll
-    for (int u = 0; u < UNR; u++) {
-      const uint32_t k = k0 + u, pos = (k << 5) + lane;
-      if (k >= nwin) break;
-      uint32_t cc = 0;
-      if (pos < tot) {
-        const uint32_t d = cs.get(key[u], key[u] - kbase);
-        cc = d - 1u;
-        if (CACHED && ((c.own[k] >> lane) & 1u)) {
-          const uint64_t c2 = choose2(d);
-          lsum += c2;
-          if (MODE == MODE_VERTEX && c2) red_add_u64(a.bv + key[u], c2);
-        }
-        BF_CHECK(MODE != MODE_EDGE || c.dlo[o[u]] + pos < a.S);
-        if (MODE == MODE_EDGE && cc) red_add_u64(a.acc + (c.dlo[o[u]] + pos), cc);  // edge (y, key)
-      }
-      if (CACHED && lane == 0) pairs += __popc(c.own[k]);
-      bool head;
-      const uint64_t rs = run_sum(c.bits[k], cc, wide, head);
-      if (head && rs) seg_add(c.slo, c.shi, o[u], rs);
-    }
+    for (int o = 1; o < G; o <<= 1) s += __shfl_xor_sync(FULL, s, o);
+    if (act && gl == 0 && s) seg_add(u.slo, u.shi, u.slot[x], s);
   }
 }
 
-template <int MODE>
-__device__ __forceinline__ void seg_flush(const CountArgs& a, const uint32_t* slo, const uint32_t* shi, bool mine,
-                                          uint32_t myj, uint32_t myy) {
+template <int MODE, int NT>
+__device__ __forceinline__ void slot_flush(const CountArgs& a, const uint32_t* slo, const uint32_t* shi, bool mine,
+                                           uint32_t myj, uint32_t myy) {
   if (!mine) return;
   const uint32_t t = threadIdx.x;
   const uint64_t v = ((uint64_t)shi[t] << 32) | slo[t];
   if (!v) return;
   BF_CHECK(myy < a.n && myj < a.S);
-  if (MODE == MODE_VERTEX) red_add_u64(a.bv + myy, v);  // centre y
-  else red_add_u64(a.acc + myj, v);                     // edge (s, y)
+  if (MODE == MODE_VERTEX) { if (!(a.exp & 2)) red_add_u64(a.bv + myy, v); }  // centre y
+  else red_add_u64(a.acc + myj, v);                                           // edge (s, y)
 }
 
-// One start on a CTA.  MULTI = false requires w <= cap and at most NT slots.
-template <int ORIENT, int MODE, bool MULTI, int NT, uint32_t CAPC, class Store>
-__device__ __forceinline__ void cta_start(const CountArgs& a, ChunkSmem<NT, CAPC>& c, const Store& cs,
-                                          const Start& st, uint64_t base, uint64_t w, uint32_t cap,
-                                          uint32_t* olist, uint64_t& lsum, uint64_t& pairs, bool& hashed) {
-  const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  constexpr uint32_t NW = NT / 32;
-  const bool wide = (st.j1 - st.j0) >= (1u << 26);  // d <= #slots: 32 * d must not wrap u32
-  if (!MULTI) {
-    bool mine;
-    uint32_t myj, myy;
-    chunk_build<MODE, NT, CAPC>(a, c, st.j0, st.j1, base, 0, cap, mine, myj, myy);
-    __syncthreads();
-    const uint32_t tot = (uint32_t)w, nwin = (tot + 31) >> 5;
-#ifdef BF_DEBUG
-    if (a.dbg_stop == 2) { for (uint32_t i = tid; i < CAPC / 32; i += NT) c.bits[i] = 0; return; }
-#endif
-    chunk_pass1<false>(a, c, cs, st.kbase, tot, nullptr, hashed);
-    __syncthreads();
-#ifdef BF_DEBUG
-    if (a.dbg_stop == 3) { for (uint32_t i = tid; i < CAPC / 32; i += NT) c.bits[i] = 0; return; }
-#endif
-    if (MODE == MODE_TOTAL) {
-      for (uint32_t k = wid; k < nwin; k += NW) {
-        BF_CHECK(k < CAPC / 32);
-        const uint32_t ow = c.own[k];
-        if ((ow >> lane) & 1u) {
-          BF_CHECK((k << 5) + lane < tot);
-          const uint32_t key = c.cache[(k << 5) + lane], kk = key - st.kbase;
-          BF_CHECK(key < a.n);
-          lsum += choose2(cs.get(key, kk));
-          cs.zero(kk);
-        }
-        if (lane == 0) pairs += __popc(ow);
-      }
-    } else {
-      chunk_pass2<MODE, true>(a, c, cs, st.kbase, tot, wide, lsum, pairs);
-      __syncthreads();
-      seg_flush<MODE>(a, c.slo, c.shi, mine, myj, myy);
-      for (uint32_t k = wid; k < nwin; k += NW)
-        if ((c.own[k] >> lane) & 1u) cs.zero(c.cache[(k << 5) + lane] - st.kbase);
-    }
-    for (uint32_t i = tid; i < nwin; i += NT) c.bits[i] = 0;
-    if (tid == 0) c.jn = FULL;
-    return;
-  }
-  // ---- multi-chunk: pass 1 over all chunks, owners to the global list
-  if (tid == 0) c.cnt = 0;
-  {
-    uint32_t jc = st.j0;
-    uint64_t K0 = 0;
-    while (K0 < w) {
-      bool mine;
-      uint32_t myj, myy;
-      const uint64_t K1 = chunk_build<MODE_TOTAL, NT, CAPC>(a, c, jc, st.j1, base, K0, cap, mine, myj, myy);
-      __syncthreads();
-      const uint32_t jn = c.jn;
-      const uint32_t tot = (uint32_t)(K1 - K0), nwin = (tot + 31) >> 5;
-      chunk_pass1<true>(a, c, cs, st.kbase, tot, olist, hashed);
-      __syncthreads();
-      for (uint32_t i = tid; i < nwin; i += NT) c.bits[i] = 0;
-      if (tid == 0) c.jn = FULL;
-      __syncthreads();
-      jc = jn != FULL ? jn : ((st.j1 - jc > (uint32_t)NT) ? jc + NT : st.j1);
-      K0 = K1;
-    }
-  }
-  const uint32_t cnt = c.cnt;
-  for (uint32_t i = tid; i < cnt; i += NT) {
-    const uint32_t key = __ldcg(olist + i), kk = key - st.kbase;
+// finalize over the owner list: C(d,2) to the total and both endpoints (total
+// mode also resets the counters here)
+template <int MODE, int NT, class Store>
+__device__ __forceinline__ void list_finalize(const CountArgs& a, const Store& cs, uint32_t kbase, uint32_t cnt,
+                                              const uint32_t* list, uint32_t lcap, const uint32_t* olist,
+                                              uint64_t& lsum) {
+  for (uint32_t i = threadIdx.x; i < cnt; i += NT) {
+    const uint32_t key = list_get(list, lcap, olist, i), kk = key - kbase;
+    BF_CHECK(key < a.n);
     const uint32_t d = cs.get(key, kk);
     if (MODE == MODE_TOTAL) cs.zero(kk);
     const uint64_t c2 = choose2(d);
     lsum += c2;
-    if (MODE == MODE_VERTEX && c2) red_add_u64(a.bv + key, c2);
+    if (MODE == MODE_VERTEX && c2 && !(a.exp & 1)) red_add_u64(a.bv + key, c2);
   }
-  if (tid == 0) pairs += cnt;
-  if (MODE == MODE_TOTAL) return;
-  __syncthreads();
-  {
-    uint32_t jc = st.j0;
-    uint64_t K0 = 0;
-    while (K0 < w) {
-      bool mine;
-      uint32_t myj, myy;
-      const uint64_t K1 = chunk_build<MODE, NT, CAPC>(a, c, jc, st.j1, base, K0, cap, mine, myj, myy);
-      __syncthreads();
-      const uint32_t jn = c.jn;
-      const uint32_t tot = (uint32_t)(K1 - K0), nwin = (tot + 31) >> 5;
-      uint64_t dummy = 0;
-      chunk_pass2<MODE, false>(a, c, cs, st.kbase, tot, wide, lsum, dummy);
-      __syncthreads();
-      seg_flush<MODE>(a, c.slo, c.shi, mine, myj, myy);
-      for (uint32_t i = tid; i < nwin; i += NT) c.bits[i] = 0;
-      if (tid == 0) c.jn = FULL;
-      __syncthreads();
-      jc = jn != FULL ? jn : ((st.j1 - jc > (uint32_t)NT) ? jc + NT : st.j1);
-      K0 = K1;
-    }
-  }
-  for (uint32_t i = tid; i < cnt; i += NT) cs.zero(__ldcg(olist + i) - st.kbase);
 }
 
-// ---------------------------------------------------------- medium tier
-struct MediumSmem {
-  ChunkSmem<MD_NT, MD_CAP> c;
-  uint32_t win[MD_WIN / 2];
-  uint32_t hk[MD_HS];
-  uint32_t hv[MD_HS];
-};
-constexpr size_t MD_SMEM = sizeof(MediumSmem);
+// One start on the CTA (all NT threads).  Single-chunk starts (w <= cap and at
+// most NT slots) build their units once for both passes; others rebuild per
+// chunk in each pass.
+template <int ORIENT, int MODE, int NT, int P, int G, uint32_t UCAP, class Store>
+__device__ __forceinline__ void unit_start(const CountArgs& a, UnitSmem<NT, P, UCAP>& u, const Store& cs,
+                                           const Start& st, uint32_t cap, uint32_t* list, uint32_t lcap,
+                                           uint32_t* olist, uint64_t& lsum, uint64_t& pairs, bool& hashed) {
+  const uint32_t tid = threadIdx.x;
+  const uint64_t base = __ldg(a.wpre + st.j0);
+  const uint64_t w = __ldg(a.wpre + st.j1) - base;
+  const bool single = w <= cap && st.j1 - st.j0 <= (uint32_t)NT;
+  bool mine = false;
+  uint32_t myj = 0, myy = 0;
+  // ---- pass 1
+  {
+    uint32_t jc = st.j0, par = 0;
+    uint64_t K0 = 0;
+    while (K0 < w) {
+      const uint64_t K1 = units_build<MODE, NT, P, UCAP>(a, u, jc, st.j1, base, K0, cap, par, mine, myj, myy);
+      const uint32_t jn = u.jn[par];
+      units_pass1<NT, P, G, UCAP>(a, u, cs, st.kbase, list, lcap, olist, hashed);
+      __syncthreads();
+      if (tid == 0) u.jn[par] = FULL;
+      jc = jn != FULL ? jn : ((st.j1 - jc > (uint32_t)NT) ? jc + NT : st.j1);
+      K0 = K1;
+      par ^= 1u;
+    }
+  }
+  const uint32_t cnt = u.lcnt;
+  list_finalize<MODE, NT>(a, cs, st.kbase, cnt, list, lcap, olist, lsum);
+  if (tid == 0) pairs += cnt;
+  if (MODE != MODE_TOTAL) {
+    __syncthreads();  // d is final
+    if (single) {
+      units_pass2<MODE, NT, P, G, UCAP>(a, u, cs, st.kbase);
+      __syncthreads();
+      slot_flush<MODE, NT>(a, u.slo, u.shi, mine, myj, myy);
+    } else {
+      uint32_t jc = st.j0, par = 0;
+      uint64_t K0 = 0;
+      while (K0 < w) {
+        const uint64_t K1 = units_build<MODE, NT, P, UCAP>(a, u, jc, st.j1, base, K0, cap, par, mine, myj, myy);
+        const uint32_t jn = u.jn[par];
+        units_pass2<MODE, NT, P, G, UCAP>(a, u, cs, st.kbase);
+        __syncthreads();
+        if (tid == 0) u.jn[par] = FULL;
+        slot_flush<MODE, NT>(a, u.slo, u.shi, mine, myj, myy);
+        jc = jn != FULL ? jn : ((st.j1 - jc > (uint32_t)NT) ? jc + NT : st.j1);
+        K0 = K1;
+        par ^= 1u;
+      }
+    }
+    for (uint32_t i = tid; i < cnt; i += NT) cs.zero(list_get(list, lcap, olist, i) - st.kbase);
+  }
+  __syncthreads();
+  if (tid == 0) u.lcnt = 0;
+}
 
-template <int ORIENT, int MODE>
-__global__ void __launch_bounds__(MD_NT) k_medium(CountArgs a) {
+// ------------------------------------------------------------- tier kernels
+// SMALL tiers (warp, medium): u16 dense window + shared hash; single chunk.
+template <int NT, uint32_t WIN, uint32_t HS, uint32_t CAP, int P, int G>
+struct SmallSmem {
+  static constexpr uint32_t UCAP = CAP / P + NT;
+  UnitSmem<NT, P, UCAP> u;
+  uint32_t win[WIN / 2];
+  uint32_t hk[HS];
+  uint32_t hv[HS];
+  uint32_t list[CAP];  // distinct keys <= w <= CAP
+};
+
+template <int ORIENT, int MODE, int NT, uint32_t WIN, uint32_t HS, uint32_t CAP, int P, int G>
+__global__ void __launch_bounds__(NT) k_small(CountArgs a) {
+  using SM = SmallSmem<NT, WIN, HS, CAP, P, G>;
   extern __shared__ __align__(16) char sm[];
-  MediumSmem& ms = *(MediumSmem*)sm;
+  SM& ss = *(SM*)sm;
   const uint32_t tid = threadIdx.x, lane = tid & 31;
+  static_assert((HS & (HS - 1)) == 0, "hash size");
   SmallStore cs;
-  cs.win = ms.win;
-  cs.hk = ms.hk;
-  cs.hv = ms.hv;
-  cs.wl = min(a.win, MD_WIN);
-  cs.hmask = MD_HS - 1;
-  cs.shift = 32 - 11;
-  static_assert(MD_HS == 2048, "hash shift");
-  for (uint32_t i = tid; i < MD_WIN / 2; i += MD_NT) ms.win[i] = 0;
-  for (uint32_t i = tid; i < MD_HS; i += MD_NT) { ms.hk[i] = EMPTY; ms.hv[i] = 0; }
-  for (uint32_t i = tid; i < MD_CAP / 32; i += MD_NT) ms.c.bits[i] = 0;
-  if (tid == 0) ms.c.jn = FULL;
+  cs.win = ss.win;
+  cs.hk = ss.hk;
+  cs.hv = ss.hv;
+  cs.wl = min(a.win, WIN);
+  cs.hmask = HS - 1;
+  cs.shift = __clz(HS) + 1;  // 32 - log2(HS)
+  for (uint32_t i = tid; i < WIN / 2; i += NT) ss.win[i] = 0;
+  for (uint32_t i = tid; i < HS; i += NT) { ss.hk[i] = EMPTY; ss.hv[i] = 0; }
+  for (uint32_t i = tid; i < UnitSmem<NT, P, SM::UCAP>::NCLS; i += NT) ss.u.ccount[i] = 0;
+  if (tid == 0) { ss.u.jn[0] = ss.u.jn[1] = FULL; ss.u.lcnt = 0; }
   uint64_t tot_acc = 0, pair_acc = 0;
   for (;;) {
-    if (tid == 0) ms.c.item = atomicAdd(a.queue, 1u);
+    if (tid == 0) ss.u.item = atomicAdd(a.queue, 1u);
     __syncthreads();
-    const uint32_t it = dealt(a, ms.c.item);
+    const uint32_t it = dealt(a, ss.u.item);
     if (it == EMPTY) break;
     const Start st = load_start<ORIENT>(a, it);
-    const uint64_t base = __ldg(a.wpre + st.j0);
-    const uint64_t w = __ldg(a.wpre + st.j1) - base;
     uint64_t lsum = 0;
     bool hashed = false;
-#ifdef BF_DEBUG
-    BF_CHECK(w <= MD_CAP && st.j1 - st.j0 <= MD_NT);
-    if (a.dbg_stop == 1) { __syncthreads(); continue; }
-#endif
-    cta_start<ORIENT, MODE, false, MD_NT, MD_CAP>(a, ms.c, cs, st, base, w, MD_CAP, nullptr, lsum, pair_acc, hashed);
+    unit_start<ORIENT, MODE, NT, P, G, SM::UCAP>(a, ss.u, cs, st, CAP, ss.list, CAP, nullptr, lsum, pair_acc,
+                                                hashed);
     tot_acc += lsum;
     if (MODE == MODE_VERTEX) {
       const uint64_t t = warp_sum(lsum);
       if (lane == 0 && t) red_add_u64(a.bv + st.s, t);
     }
     if (__syncthreads_or(hashed))
-      for (uint32_t i = tid; i < MD_HS; i += MD_NT) { ms.hk[i] = EMPTY; ms.hv[i] = 0; }
+      for (uint32_t i = tid; i < HS; i += NT) { ss.hk[i] = EMPTY; ss.hv[i] = 0; }
   }
   flush_totals(a, tot_acc, pair_acc);
 }
 
-// ----------------------------------------------------------- heavy tier
-struct HeavySmem {
-  ChunkSmem<HV_NT, HV_CAP> c;
-  uint32_t win[HV_WIN];
+// HEAVY tier: u32 dense window + per-CTA global overflow row; chunked.
+template <int NT, uint32_t WIN, uint32_t CAP, uint32_t LCAP, int P, int G>
+struct HeavySmemT {
+  static constexpr uint32_t UCAP = CAP / P + NT;
+  UnitSmem<NT, P, UCAP> u;
+  uint32_t win[WIN];
+  uint32_t list[LCAP];
 };
-constexpr size_t HV_SMEM = sizeof(HeavySmem);
 
-template <int ORIENT, int MODE>
-__global__ void __launch_bounds__(HV_NT) k_heavy(CountArgs a) {
+template <int ORIENT, int MODE, int NT, uint32_t WIN, uint32_t CAP, uint32_t LCAP, int P, int G>
+__global__ void __launch_bounds__(NT) k_big(CountArgs a) {
+  using SM = HeavySmemT<NT, WIN, CAP, LCAP, P, G>;
   extern __shared__ __align__(16) char sm[];
-  HeavySmem& hs = *(HeavySmem*)sm;
+  SM& hs = *(SM*)sm;
   const uint32_t tid = threadIdx.x, lane = tid & 31;
   HeavyStore cs;
   cs.win = hs.win;
   cs.orow = a.orow + (size_t)blockIdx.x * a.orow_len;
+  cs.wl = min(a.win, WIN);
   cs.lenchk = a.orow_len;
-  cs.wl = min(a.win, HV_WIN);
   uint32_t* olist = a.olist + (size_t)blockIdx.x * a.orow_len;
-  const uint32_t cap = min(a.cap, HV_CAP);
-  for (uint32_t i = tid; i < HV_WIN; i += HV_NT) hs.win[i] = 0;
-  for (uint32_t i = tid; i < HV_CAP / 32; i += HV_NT) hs.c.bits[i] = 0;
-  if (tid == 0) hs.c.jn = FULL;
+  const uint32_t cap = min(a.cap, CAP);
+  for (uint32_t i = tid; i < WIN; i += NT) hs.win[i] = 0;
+  for (uint32_t i = tid; i < UnitSmem<NT, P, SM::UCAP>::NCLS; i += NT) hs.u.ccount[i] = 0;
+  if (tid == 0) { hs.u.jn[0] = hs.u.jn[1] = FULL; hs.u.lcnt = 0; }
   uint64_t tot_acc = 0, pair_acc = 0;
   for (;;) {
-    if (tid == 0) hs.c.item = atomicAdd(a.queue, 1u);
+    if (tid == 0) hs.u.item = atomicAdd(a.queue, 1u);
     __syncthreads();
-    const uint32_t it = dealt(a, hs.c.item);
+    const uint32_t it = dealt(a, hs.u.item);
     if (it == EMPTY) break;
     const Start st = load_start<ORIENT>(a, it);
-    const uint64_t base = __ldg(a.wpre + st.j0);
-    const uint64_t w = __ldg(a.wpre + st.j1) - base;
     uint64_t lsum = 0;
     bool hashed = false;
-    if (w <= cap && st.j1 - st.j0 <= (uint32_t)HV_NT)
-      cta_start<ORIENT, MODE, false, HV_NT, HV_CAP>(a, hs.c, cs, st, base, w, cap, olist, lsum, pair_acc, hashed);
-    else
-      cta_start<ORIENT, MODE, true, HV_NT, HV_CAP>(a, hs.c, cs, st, base, w, cap, olist, lsum, pair_acc, hashed);
+    unit_start<ORIENT, MODE, NT, P, G, SM::UCAP>(a, hs.u, cs, st, cap, hs.list, LCAP, olist, lsum, pair_acc,
+                                                hashed);
     tot_acc += lsum;
     if (MODE == MODE_VERTEX) {
       const uint64_t t = warp_sum(lsum);
       if (lane == 0 && t) red_add_u64(a.bv + st.s, t);
     }
-    __syncthreads();
   }
   flush_totals(a, tot_acc, pair_acc);
 }
+
+// tier configurations
+// warp tier: 1-warp CTAs, w <= 512, <= 32 slots
+#define WARP_CFG 32, 4096, 512, BF_WARP_MAX_WEDGES, 8, 4
+using WarpSM = SmallSmem<WARP_CFG>;
+// medium tier: 128 threads, w <= 2048, <= 128 slots
+#define MED_CFG 128, 8192, 2048, BF_MEDIUM_MAX_WEDGES, 16, 4
+using MedSM = SmallSmem<MED_CFG>;
+// heavy tier: 256 threads, chunks of <= 8192 wedges
+#define BIG_CFG 256, 8192, 8192, 4096, 32, 4
+using BigSM = HeavySmemT<BIG_CFG>;
+static_assert(BF_WARP_MAX_SLOTS == 32 && BF_MEDIUM_MAX_SLOTS == 128, "tier slot bounds = CTA sizes");
 
 // ============================================================ output kernels
 __global__ void k_unrename(const uint64_t* __restrict__ bv, const uint32_t* __restrict__ rid_of_gid, uint32_t nU,
@@ -795,30 +621,32 @@ int occupancy(K kernel, int threads, size_t smem) {
   return b > 0 ? b : 1;
 }
 
-int heavy_grid(int sms) { return sms * occupancy(k_heavy<BF_ORIENT_HIGH, MODE_VERTEX>, HV_NT, HV_SMEM); }
+int heavy_grid(int sms) {
+  return sms * occupancy(k_big<BF_ORIENT_HIGH, MODE_VERTEX, BIG_CFG>, 256, sizeof(BigSM));
+}
 
 template <int ORIENT, int MODE>
 void launch_tiers(bf_graph* g, CountArgs a, const uint32_t tier[4], uint32_t* queues, cudaStream_t s) {
   const int sms = g->sms;
   if (tier[1] > tier[0]) {  // heavy
-    auto k = k_heavy<ORIENT, MODE>;
-    const int grid = sms * occupancy(k, HV_NT, HV_SMEM);
+    auto k = k_big<ORIENT, MODE, BIG_CFG>;
+    const int grid = sms * occupancy(k, 256, sizeof(BigSM));
     a.t0 = tier[0]; a.t1 = tier[1]; a.queue = queues + 0;
-    k<<<grid, HV_NT, HV_SMEM, s>>>(a);
+    k<<<grid, 256, sizeof(BigSM), s>>>(a);
     KERNEL_CHECK(g);
   }
   if (tier[2] > tier[1]) {  // medium
-    auto k = k_medium<ORIENT, MODE>;
-    const int grid = sms * occupancy(k, MD_NT, MD_SMEM);
+    auto k = k_small<ORIENT, MODE, MED_CFG>;
+    const int grid = sms * occupancy(k, 128, sizeof(MedSM));
     a.t0 = tier[1]; a.t1 = tier[2]; a.queue = queues + 1;
-    k<<<grid, MD_NT, MD_SMEM, s>>>(a);
+    k<<<grid, 128, sizeof(MedSM), s>>>(a);
     KERNEL_CHECK(g);
   }
   if (tier[3] > tier[2]) {  // warp
-    auto k = k_warp<ORIENT, MODE>;
-    const int grid = sms * occupancy(k, WT_WARPS * 32, WT_SMEM);
+    auto k = k_small<ORIENT, MODE, WARP_CFG>;
+    const int grid = sms * occupancy(k, 32, sizeof(WarpSM));
     a.t0 = tier[2]; a.t1 = tier[3]; a.queue = queues + 2;
-    k<<<grid, WT_WARPS * 32, WT_SMEM, s>>>(a);
+    k<<<grid, 32, sizeof(WarpSM), s>>>(a);
     KERNEL_CHECK(g);
   }
 }
@@ -844,7 +672,7 @@ bf_status graph_count(bf_graph* g, int mode, uint64_t* out_a, uint64_t* out_b, u
   // key offset (< max side size); rows stay zero between starts (owners reset
   // them), so they are cleared once when allocated
   const uint32_t win = (g->opt.test_flags & BF_FLAG_SMALL_WINDOW) ? 64u : 0xFFFFFFFFu;
-  const uint32_t cap = (g->opt.test_flags & BF_FLAG_SMALL_CHUNK) ? 64u : HV_CAP;
+  const uint32_t cap = (g->opt.test_flags & BF_FLAG_SMALL_CHUNK) ? 64u : 0xFFFFFFFFu;
   const uint64_t olen = std::max<uint64_t>(std::max(g->n_u, g->n_v), 1);
   if (g->n_tier[0]) {
     const size_t rows = (size_t)heavy_grid(g->sms);
@@ -867,6 +695,7 @@ bf_status graph_count(bf_graph* g, int mode, uint64_t* out_a, uint64_t* out_b, u
   a.orow_len = olen;
   a.S = S;
   a.n = n;
+  a.exp = getenv("BF_EXPERIMENT") ? (uint32_t)atoi(getenv("BF_EXPERIMENT")) : 0u;
   a.dbg_stop = getenv("BF_DBG_STOP") ? (uint32_t)atoi(getenv("BF_DBG_STOP")) : 0u;
   a.n_u = g->n_u;
   a.n_v = g->n_v;

@@ -30,9 +30,13 @@ def main():
               for orient in ("high", "low"):
                   cases.append(dict(g=gspec, mode=mode, flags=flags, orient=orient, rank="degree"))
   for c in cases:
-      r = subprocess.run([sys.executable, "-c", CHILD, json.dumps(c)], capture_output=True, text=True, timeout=120)
-      out = (r.stdout + r.stderr)
-      res = "ok" if "RESULT ok" in out else ("mismatch" if "RESULT mismatch" in out else "ERROR")
+      try:
+          r = subprocess.run([sys.executable, "-c", CHILD, json.dumps(c)], capture_output=True, text=True, timeout=60)
+          out = (r.stdout + r.stderr)
+      except subprocess.TimeoutExpired:
+          out = "TIMEOUT"
+      res = "ok" if "RESULT ok" in out else ("mismatch" if "RESULT mismatch" in out else
+                                             ("TIMEOUT" if out == "TIMEOUT" else "ERROR"))
       extra = [l for l in out.splitlines() if "BF_CHECK" in l or "BFError" in l][:2]
       print(res, json.dumps(c), " | ".join(extra)[:300], flush=True)
 
