@@ -58,8 +58,10 @@ struct CountArgs {
   const uint32_t* nbr;
   const uint64_t* wpre;   // [2m+1] per-slot wedge prefix
   const uint32_t* seglo;  // [2m]   per-slot segment start in nbr
+  const uint32_t* seglen; // [2m]   per-slot segment length (wedges through the slot)
   const uint4* items;     // planned starts {s, j0, j1, -}, sorted by (tier, wedges desc)
   uint64_t* bv;           // [n+1] per-vertex (rid space)
+  uint64_t* hub;          // [HUB_STRIPES][2][HUB_KEYS] striped endpoint sums of hub keys (vertex mode)
   uint64_t* acc;          // [2m] per-slot (edge mode)
   uint64_t* total;        // [0] total, [1] distinct pairs
   uint32_t* orow;         // heavy: per-CTA overflow rows (indexed by key offset)
@@ -76,17 +78,6 @@ struct CountArgs {
   uint32_t cap;           // heavy chunk capacity in wedges (<= HV_CAP)
   int rank, world;
 };
-
-__device__ __forceinline__ uint32_t lanemask_lt() {
-  uint32_t r;
-  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ uint32_t lanemask_le() {
-  uint32_t r;
-  asm("mov.u32 %0, %%lanemask_le;" : "=r"(r));
-  return r;
-}
 
 // q-th start of this rank inside the tier segment (snake deal over the
 // wedge-sorted list: round q takes q*G + (q odd ? G-1-r : r)); EMPTY if none
@@ -114,24 +105,6 @@ __device__ __forceinline__ Start load_start(const CountArgs& a, uint32_t it) {
   return t;
 }
 
-// Sum v over the lane's run inside a window (runs start at segment starts and
-// at lane 0).  `wide` (d may reach 2^27) sums 16-bit halves so nothing wraps.
-__device__ __forceinline__ uint64_t run_sum(uint32_t starts, uint32_t v, bool wide, bool& head) {
-  const uint32_t lane = threadIdx.x & 31;
-  const uint32_t heads = starts | 1u;
-  const uint32_t le = lanemask_le();
-  const uint32_t first = 31 - __clz(heads & le);
-  const uint32_t after = heads & ~le;
-  const uint32_t end = after ? (uint32_t)(__ffs(after) - 1) : 32u;
-  const uint32_t rm = (end == 32u ? FULL : ((1u << end) - 1u)) & ~((1u << first) - 1u);
-  head = lane == first;
-  BF_CHECK(__activemask() == FULL);
-  if (!wide) return __reduce_add_sync(rm, v);
-  const uint32_t lo = __reduce_add_sync(rm, v & 0xffffu);
-  const uint32_t hi = __reduce_add_sync(rm, v >> 16);
-  return (uint64_t)lo + ((uint64_t)hi << 16);
-}
-
 // u64 add into a (lo, hi) pair of u32 shared counters (native 32-bit shared
 // atomics; a 64-bit shared atomicAdd compiles to a CAS loop)
 __device__ __forceinline__ void seg_add(uint32_t* slo, uint32_t* shi, uint32_t o, uint64_t v) {
@@ -150,13 +123,29 @@ __device__ __forceinline__ void flush_totals(const CountArgs& a, uint64_t tot_ac
   }
 }
 
+// Endpoint contributions C(d,2) land on the aggregated keys, which in the
+// HIGH orientation are the few highest-ranked vertices of each side: one
+// address per hub hammered by every CTA.  Keys among the first HUB_KEYS rids
+// of their side therefore go to one of HUB_STRIPES striped copies (chosen by
+// CTA), summed into bv by k_hub_reduce after the wedge kernels.
+constexpr uint32_t HUB_KEYS = 4096;
+constexpr uint32_t HUB_STRIPES = 16;
+__device__ __forceinline__ uint64_t* endpoint_slot(const CountArgs& a, uint32_t key) {
+  const uint32_t side = key >= a.n_u, kk = key - (side ? a.n_u : 0u);
+  if (kk < HUB_KEYS)
+    return a.hub + ((size_t)(blockIdx.x & (HUB_STRIPES - 1)) * 2 + side) * HUB_KEYS + kk;
+  return a.bv + key;
+}
+
 // ------------------------------------------------ small counter store
-// u16 dense window over key offsets [0, wl) + open-addressed hash (u32 keys,
-// u32 counts) for the rest.  d <= w <= 2048 here, so u16 never wraps.
+// u8 dense window over key offsets [0, wl) + open-addressed hash (u32 keys,
+// u32 counts) for the rest.  In the small tiers d(s,x) <= #slots of s <= 128
+// (each centre y in N(s) contributes at most one wedge per key), so u8 never
+// wraps.
 __device__ __forceinline__ uint32_t hslot(uint32_t key, uint32_t shift) { return (key * 0x9E3779B1u) >> shift; }
 
 struct SmallStore {
-  uint32_t* win;  // u16 counters, two per word
+  uint32_t* win;  // u8 counters, four per word
   uint32_t* hk;
   uint32_t* hv;
   uint32_t wl, hmask, shift;
@@ -164,27 +153,22 @@ struct SmallStore {
   // returns true if this increment took the key's count from 0 to 1
   __device__ __forceinline__ bool add(uint32_t key, uint32_t kk, bool& hashed) const {
     if (kk < wl) {
-      BF_CHECK((kk >> 1) < (hmask + 1) * 4 && __isShared(win + (kk >> 1)));
-      const uint32_t sh = (kk & 1u) << 4;
-      const uint32_t old = atomicAdd(win + (kk >> 1), 1u << sh);
-      return ((old >> sh) & 0xffffu) == 0u;
+      BF_CHECK(__isShared(win + (kk >> 2)));
+      const uint32_t sh = (kk & 3u) << 3;
+      const uint32_t old = atomicAdd(win + (kk >> 2), 1u << sh);
+      return ((old >> sh) & 0xffu) == 0u;
     }
     hashed = true;
     uint32_t h = hslot(key, shift);
-    BF_CHECK(h <= hmask);
     for (uint32_t probes = 0;; probes++) {
       if (probes > hmask) __trap();  // more distinct keys than slots: impossible by the tier bound
-      uint32_t cur = ((volatile uint32_t*)hk)[h];
-      if (cur == EMPTY) {
-        cur = atomicCAS(hk + h, EMPTY, key);
-        if (cur == EMPTY) cur = key;
-      }
-      if (cur == key) return atomicAdd(hv + h, 1u) == 0u;
+      const uint32_t cur = atomicCAS(hk + h, EMPTY, key);
+      if (cur == EMPTY || cur == key) return atomicAdd(hv + h, 1u) == 0u;
       h = (h + 1) & hmask;
     }
   }
   __device__ __forceinline__ uint32_t get(uint32_t key, uint32_t kk) const {
-    if (kk < wl) return ((const uint16_t*)win)[kk];
+    if (kk < wl) return ((const uint8_t*)win)[kk];
     uint32_t h = hslot(key, shift);
     for (uint32_t probes = 0; hk[h] != key; probes++) {
       if (probes > hmask) __trap();  // the key was inserted in pass 1
@@ -193,7 +177,7 @@ struct SmallStore {
     return hv[h];
   }
   __device__ __forceinline__ void zero(uint32_t kk) const {  // window keys only; the hash is cleared whole
-    if (kk < wl) ((uint16_t*)win)[kk] = 0;
+    if (kk < wl) ((uint8_t*)win)[kk] = 0;
   }
 };
 
@@ -220,39 +204,70 @@ struct HeavyStore {
 };
 
 // ================================================================ unit walk
-// A chunk of a start's wedge sequence (at most NT slots, at most CAP wedges)
-// is cut into "units": pieces of at most P consecutive wedges of one segment.
-// Units are bucketed by length (full pieces first, then halving lengths) so the
-// G-lane groups of a warp walk units of similar length; each lane of a group
-// reads every G-th key of its unit (P/G independent loads in flight per lane).
-// Pass-2 sums of d-1 stay in registers until one shared atomic per unit.
-template <int NT, int P, uint32_t UCAP>
-struct UnitSmem {
-  static constexpr int NCLS = 1 + (P >= 2) + (P >= 4) + (P >= 8) + (P >= 16) + (P >= 32) + (P >= 64);
+// A chunk of a start's wedge sequence is cut into "units": pieces of at most P
+// consecutive wedges of one segment, numbered in slot order by a scan of the
+// per-slot unit counts.  A G-lane group walks one unit per round, each lane
+// reading every G-th key (P/G predicated loads in flight per lane, UR units per
+// group unrolled), so no lane ever searches for its segment.  Pass-2 sums of
+// d-1 stay in registers until one shared atomic per unit.
+template <int NT, uint32_t UCAP>
+struct Units {
   using SlotT = typename std::conditional<(NT <= 256), uint8_t, uint16_t>::type;
   uint32_t lo[UCAP];           // first nbr index of the unit
   uint8_t len[UCAP];           // 1..P
   SlotT slot[UCAP];            // chunk-local slot (thread) of the unit
   uint32_t slo[NT], shi[NT];   // pass-2 per-slot sums (u64 as two u32)
-  uint32_t ccount[NCLS], cstart[NCLS];
+  uint32_t wt[32];             // scan scratch
   uint32_t jn[2];              // continuation slot of chunk i in jn[i & 1] (FULL = none)
   uint32_t nunits, item, lcnt;
 };
 
-// length class: 0 = full (len == P); c = log2(P) - floor(log2(len)) otherwise
-template <int P>
-__device__ __forceinline__ uint32_t len_class(uint32_t len) {
-  return len >= (uint32_t)P ? 0u : (uint32_t)(31 - __clz(P)) - (uint32_t)(31 - __clz(len));
+// exclusive scan of v over the CTA (NT == 32: one warp, no CTA barrier)
+template <int NT>
+__device__ __forceinline__ uint32_t cta_scan(uint32_t v, uint32_t* wt, uint32_t& total) {
+  if (NT == 32) {
+    const uint32_t inc = warp_inclusive_scan(v);
+    total = __shfl_sync(FULL, inc, 31);
+    return inc - v;
+  }
+  uint32_t t;
+  const uint32_t ex = block_exclusive_scan<uint32_t>(v, wt, &t);
+  total = t;
+  return ex;
+}
+
+template <int NT>
+__device__ __forceinline__ void cta_sync() {
+  if (NT == 32) __syncwarp();
+  else __syncthreads();
+}
+
+// write the units of one slot segment [lo, lo+L) (thread t), then barrier
+template <int NT, int P, uint32_t UCAP>
+__device__ __forceinline__ void units_write(Units<NT, UCAP>& u, uint32_t lo, uint32_t L) {
+  constexpr uint32_t LP = 31 - __builtin_clz(P);
+  const uint32_t nu = (L + P - 1) >> LP;
+  uint32_t total;
+  const uint32_t ex = cta_scan<NT>(nu, u.wt, total);
+  BF_CHECK(ex + nu <= UCAP);
+  for (uint32_t f = 0; f < nu; f++) {
+    u.lo[ex + f] = lo + (f << LP);
+    u.len[ex + f] = (uint8_t)min(L - (f << LP), (uint32_t)P);
+    u.slot[ex + f] = (typename Units<NT, UCAP>::SlotT)threadIdx.x;
+  }
+  if (threadIdx.x == 0) u.nunits = total;
+  u.slo[threadIdx.x] = 0;
+  u.shi[threadIdx.x] = 0;
+  cta_sync<NT>();
 }
 
 // Build the units of chunk [K0, K1) of the start's wedges from slots
-// [jc, min(jc+NT, j1)).  Thread t handles slot jc + t; `mine` = it has a
-// segment in the chunk.  Returns K1; u.jn[par] receives the slot that
+// [jc, min(jc+NT, j1)) (heavy tier).  Thread t handles slot jc + t; `mine` =
+// it has a segment in the chunk.  Returns K1; u.jn[par] receives the slot that
 // continues past K1 (if any; the caller resets it after reading, and chunks
-// alternate par so the reset never races the next chunk's write).  Three CTA
-// barriers.
+// alternate par so the reset never races the next chunk's write).
 template <int MODE, int NT, int P, uint32_t UCAP>
-__device__ __forceinline__ uint64_t units_build(const CountArgs& a, UnitSmem<NT, P, UCAP>& u, uint32_t jc, uint32_t j1,
+__device__ __forceinline__ uint64_t units_build(const CountArgs& a, Units<NT, UCAP>& u, uint32_t jc, uint32_t j1,
                                                 uint64_t base, uint64_t K0, uint32_t cap, uint32_t par, bool& mine,
                                                 uint32_t& myj, uint32_t& myy) {
   const uint32_t tid = threadIdx.x;
@@ -274,43 +289,9 @@ __device__ __forceinline__ uint64_t units_build(const CountArgs& a, UnitSmem<NT,
       lo = __ldg(a.seglo + j) + (uint32_t)(a0 - A);
       mine = true;
       if (MODE == MODE_VERTEX) myy = __ldg(a.nbr + j);
-      if (MODE != MODE_TOTAL) { u.slo[tid] = 0; u.shi[tid] = 0; }
     }
   }
-  constexpr uint32_t LP = 31 - __builtin_clz(P);
-  const uint32_t nf = L >> LP, r = L & (P - 1);
-  const uint32_t cr = r ? len_class<P>(r) : 0u;
-  uint32_t bf = 0, br = 0;
-  if (nf) bf = atomicAdd(&u.ccount[0], nf);
-  if (r) br = atomicAdd(&u.ccount[cr], 1u);
-  __syncthreads();
-  if (tid == 0) {
-    uint32_t s = 0;
-#pragma unroll
-    for (int c = 0; c < UnitSmem<NT, P, UCAP>::NCLS; c++) {
-      u.cstart[c] = s;
-      s += u.ccount[c];
-      u.ccount[c] = 0;
-    }
-    u.nunits = s;
-    BF_CHECK(s <= UCAP);
-  }
-  __syncthreads();
-  if (L) {
-    const uint32_t b0 = u.cstart[0] + bf;
-    for (uint32_t f = 0; f < nf; f++) {
-      u.lo[b0 + f] = lo + (f << LP);
-      u.len[b0 + f] = (uint8_t)P;
-      u.slot[b0 + f] = (typename UnitSmem<NT, P, UCAP>::SlotT)tid;
-    }
-    if (r) {
-      const uint32_t ur = u.cstart[cr] + br;
-      u.lo[ur] = lo + (nf << LP);
-      u.len[ur] = (uint8_t)r;
-      u.slot[ur] = (typename UnitSmem<NT, P, UCAP>::SlotT)tid;
-    }
-  }
-  __syncthreads();
+  units_write<NT, P, UCAP>(u, lo, L);
   return K1;
 }
 
@@ -330,29 +311,37 @@ __device__ __forceinline__ uint32_t list_get(const uint32_t* list, uint32_t lcap
 }
 
 // pass 1 over the chunk's units: d(key) += 1 per wedge
-template <int NT, int P, int G, uint32_t UCAP, class Store>
-__device__ __forceinline__ void units_pass1(const CountArgs& a, UnitSmem<NT, P, UCAP>& u, const Store& cs,
+template <int NT, int P, int G, int UR, uint32_t UCAP, class Store>
+__device__ __forceinline__ void units_pass1(const CountArgs& a, Units<NT, UCAP>& u, const Store& cs,
                                             uint32_t kbase, uint32_t* list, uint32_t lcap, uint32_t* olist,
                                             bool& hashed) {
   constexpr int IT = P / G;
+  constexpr uint32_t NG = NT / G;
   const uint32_t tid = threadIdx.x, gl = tid & (G - 1);
   const uint32_t nunits = u.nunits;
-  for (uint32_t x = tid / G; x < nunits; x += NT / G) {
-    const uint32_t lo = u.lo[x], len = u.len[x];
-    uint32_t key[IT];
+  for (uint32_t x0 = tid / G; x0 < nunits; x0 += NG * UR) {
+    uint32_t key[UR][IT];
 #pragma unroll
-    for (int it = 0; it < IT; it++) {
-      const uint32_t i = gl + it * G;
-      BF_CHECK(i >= len || lo + i < a.S);
-      key[it] = i < len ? __ldg(a.nbr + (lo + i)) : EMPTY;
-    }
+    for (int r = 0; r < UR; r++) {
+      const uint32_t x = x0 + r * NG;
+      const uint32_t lo = x < nunits ? u.lo[x] : 0u, len = x < nunits ? u.len[x] : 0u;
 #pragma unroll
-    for (int it = 0; it < IT; it++) {
-      if (key[it] != EMPTY) {
-        BF_CHECK(key[it] < a.n);
-        if (cs.add(key[it], key[it] - kbase, hashed)) list_push(&u.lcnt, list, lcap, olist, a.orow_len, key[it]);
+      for (int it = 0; it < IT; it++) {
+        const uint32_t i = gl + it * G;
+        BF_CHECK(i >= len || lo + i < a.S);
+        key[r][it] = i < len ? __ldg(a.nbr + (lo + i)) : EMPTY;
       }
     }
+#pragma unroll
+    for (int r = 0; r < UR; r++)
+#pragma unroll
+      for (int it = 0; it < IT; it++) {
+        const uint32_t k = key[r][it];
+        if (k != EMPTY) {
+          BF_CHECK(k < a.n);
+          if (cs.add(k, k - kbase, hashed)) list_push(&u.lcnt, list, lcap, olist, a.orow_len, k);
+        }
+      }
   }
 }
 
@@ -360,7 +349,7 @@ __device__ __forceinline__ void units_pass1(const CountArgs& a, UnitSmem<NT, P, 
 // (centre y in vertex mode, edge (s, y) in edge mode); edge mode also adds c
 // to the wedge's (y, key) edge
 template <int MODE, int NT, int P, int G, uint32_t UCAP, class Store>
-__device__ __forceinline__ void units_pass2(const CountArgs& a, UnitSmem<NT, P, UCAP>& u, const Store& cs,
+__device__ __forceinline__ void units_pass2(const CountArgs& a, Units<NT, UCAP>& u, const Store& cs,
                                             uint32_t kbase) {
   constexpr int IT = P / G;
   const uint32_t tid = threadIdx.x, gl = tid & (G - 1);
@@ -391,7 +380,7 @@ __device__ __forceinline__ void units_pass2(const CountArgs& a, UnitSmem<NT, P, 
   }
 }
 
-template <int MODE, int NT>
+template <int MODE>
 __device__ __forceinline__ void slot_flush(const CountArgs& a, const uint32_t* slo, const uint32_t* shi, bool mine,
                                            uint32_t myj, uint32_t myy) {
   if (!mine) return;
@@ -416,35 +405,35 @@ __device__ __forceinline__ void list_finalize(const CountArgs& a, const Store& c
     if (MODE == MODE_TOTAL) cs.zero(kk);
     const uint64_t c2 = choose2(d);
     lsum += c2;
-    if (MODE == MODE_VERTEX && c2 && !(a.exp & 1)) red_add_u64(a.bv + key, c2);
+    if (MODE == MODE_VERTEX && c2 && !(a.exp & 1)) red_add_u64(endpoint_slot(a, key), c2);
   }
 }
 
-// One start on the CTA (all NT threads).  Single-chunk starts (w <= cap and at
-// most NT slots) build their units once for both passes; others rebuild per
-// chunk in each pass.
-template <int ORIENT, int MODE, int NT, int P, int G, uint32_t UCAP, class Store>
-__device__ __forceinline__ void unit_start(const CountArgs& a, UnitSmem<NT, P, UCAP>& u, const Store& cs,
-                                           const Start& st, uint32_t cap, uint32_t* list, uint32_t lcap,
-                                           uint32_t* olist, uint64_t& lsum, uint64_t& pairs, bool& hashed) {
+// The rest of a start once its (first) chunk's units are built: pass 1,
+// finalize, pass 2, reset.  `single`: the whole start is that one chunk
+// (units reused by pass 2); otherwise chunks are rebuilt by units_build.
+template <int ORIENT, int MODE, int NT, int P, int G, int UR, uint32_t UCAP, class Store>
+__device__ __forceinline__ void start_passes(const CountArgs& a, Units<NT, UCAP>& u, const Store& cs,
+                                             const Start& st, bool single, uint64_t base, uint64_t w, uint64_t K1,
+                                             uint32_t cap, uint32_t jn0, bool mine, uint32_t myj, uint32_t myy,
+                                             uint32_t* list, uint32_t lcap, uint32_t* olist, uint64_t& lsum,
+                                             uint64_t& pairs, bool& hashed) {
   const uint32_t tid = threadIdx.x;
-  const uint64_t base = __ldg(a.wpre + st.j0);
-  const uint64_t w = __ldg(a.wpre + st.j1) - base;
-  const bool single = w <= cap && st.j1 - st.j0 <= (uint32_t)NT;
-  bool mine = false;
-  uint32_t myj = 0, myy = 0;
-  // ---- pass 1
-  {
-    uint32_t jc = st.j0, par = 0;
-    uint64_t K0 = 0;
+  // ---- pass 1 (first chunk already built)
+  units_pass1<NT, P, G, UR, UCAP>(a, u, cs, st.kbase, list, lcap, olist, hashed);
+  cta_sync<NT>();
+  if (!single) {
+    if (tid == 0) u.jn[0] = FULL;
+    uint32_t jc = jn0 != FULL ? jn0 : ((st.j1 - st.j0 > (uint32_t)NT) ? st.j0 + NT : st.j1), par = 1;
+    uint64_t K0 = K1;
     while (K0 < w) {
-      const uint64_t K1 = units_build<MODE, NT, P, UCAP>(a, u, jc, st.j1, base, K0, cap, par, mine, myj, myy);
+      const uint64_t Kn = units_build<MODE, NT, P, UCAP>(a, u, jc, st.j1, base, K0, cap, par, mine, myj, myy);
       const uint32_t jn = u.jn[par];
-      units_pass1<NT, P, G, UCAP>(a, u, cs, st.kbase, list, lcap, olist, hashed);
-      __syncthreads();
+      units_pass1<NT, P, G, UR, UCAP>(a, u, cs, st.kbase, list, lcap, olist, hashed);
+      cta_sync<NT>();
       if (tid == 0) u.jn[par] = FULL;
       jc = jn != FULL ? jn : ((st.j1 - jc > (uint32_t)NT) ? jc + NT : st.j1);
-      K0 = K1;
+      K0 = Kn;
       par ^= 1u;
     }
   }
@@ -452,51 +441,70 @@ __device__ __forceinline__ void unit_start(const CountArgs& a, UnitSmem<NT, P, U
   list_finalize<MODE, NT>(a, cs, st.kbase, cnt, list, lcap, olist, lsum);
   if (tid == 0) pairs += cnt;
   if (MODE != MODE_TOTAL) {
-    __syncthreads();  // d is final
+    cta_sync<NT>();  // d is final
     if (single) {
       units_pass2<MODE, NT, P, G, UCAP>(a, u, cs, st.kbase);
-      __syncthreads();
-      slot_flush<MODE, NT>(a, u.slo, u.shi, mine, myj, myy);
+      cta_sync<NT>();
+      slot_flush<MODE>(a, u.slo, u.shi, mine, myj, myy);
     } else {
       uint32_t jc = st.j0, par = 0;
       uint64_t K0 = 0;
       while (K0 < w) {
-        const uint64_t K1 = units_build<MODE, NT, P, UCAP>(a, u, jc, st.j1, base, K0, cap, par, mine, myj, myy);
+        const uint64_t Kn = units_build<MODE, NT, P, UCAP>(a, u, jc, st.j1, base, K0, cap, par, mine, myj, myy);
         const uint32_t jn = u.jn[par];
         units_pass2<MODE, NT, P, G, UCAP>(a, u, cs, st.kbase);
-        __syncthreads();
+        cta_sync<NT>();
         if (tid == 0) u.jn[par] = FULL;
-        slot_flush<MODE, NT>(a, u.slo, u.shi, mine, myj, myy);
+        slot_flush<MODE>(a, u.slo, u.shi, mine, myj, myy);
         jc = jn != FULL ? jn : ((st.j1 - jc > (uint32_t)NT) ? jc + NT : st.j1);
-        K0 = K1;
+        K0 = Kn;
         par ^= 1u;
       }
     }
     for (uint32_t i = tid; i < cnt; i += NT) cs.zero(list_get(list, lcap, olist, i) - st.kbase);
   }
-  __syncthreads();
+  cta_sync<NT>();
   if (tid == 0) u.lcnt = 0;
 }
 
-// ------------------------------------------------------------- tier kernels
-// SMALL tiers (warp, medium): u16 dense window + shared hash; single chunk.
-template <int NT, uint32_t WIN, uint32_t HS, uint32_t CAP, int P, int G>
+// ------------------------------------------------------------- small tiers
+// warp / medium: u8 dense window + shared hash; one chunk per start (w <= CAP,
+// slots <= NT).  Starts are taken in a static stride (the tier is sorted by
+// wedges, so neighbours in the stride are alike) with a two-stage register
+// prefetch: the item two starts ahead and the slot data one start ahead are in
+// flight while the current start runs.
+template <int NT, uint32_t WIN, uint32_t HS, uint32_t CAP, int P, int G, int UR>
 struct SmallSmem {
   static constexpr uint32_t UCAP = CAP / P + NT;
-  UnitSmem<NT, P, UCAP> u;
-  uint32_t win[WIN / 2];
+  Units<NT, UCAP> u;
+  uint32_t win[WIN / 4];
   uint32_t hk[HS];
   uint32_t hv[HS];
   uint32_t list[CAP];  // distinct keys <= w <= CAP
 };
 
-template <int ORIENT, int MODE, int NT, uint32_t WIN, uint32_t HS, uint32_t CAP, int P, int G>
+struct SlotRegs {
+  uint32_t lo, len, y;
+};
+
+template <int MODE>
+__device__ __forceinline__ SlotRegs load_slot(const CountArgs& a, uint32_t j, uint32_t j1) {
+  SlotRegs r{0u, 0u, 0u};
+  if (j < j1) {
+    r.lo = __ldg(a.seglo + j);
+    r.len = __ldg(a.seglen + j);
+    if (MODE == MODE_VERTEX) r.y = __ldg(a.nbr + j);
+  }
+  return r;
+}
+
+template <int ORIENT, int MODE, int NT, uint32_t WIN, uint32_t HS, uint32_t CAP, int P, int G, int UR>
 __global__ void __launch_bounds__(NT) k_small(CountArgs a) {
-  using SM = SmallSmem<NT, WIN, HS, CAP, P, G>;
+  using SM = SmallSmem<NT, WIN, HS, CAP, P, G, UR>;
   extern __shared__ __align__(16) char sm[];
   SM& ss = *(SM*)sm;
   const uint32_t tid = threadIdx.x, lane = tid & 31;
-  static_assert((HS & (HS - 1)) == 0, "hash size");
+  static_assert((HS & (HS - 1)) == 0 && WIN % 4 == 0, "store sizes");
   SmallStore cs;
   cs.win = ss.win;
   cs.hk = ss.hk;
@@ -504,44 +512,72 @@ __global__ void __launch_bounds__(NT) k_small(CountArgs a) {
   cs.wl = min(a.win, WIN);
   cs.hmask = HS - 1;
   cs.shift = __clz(HS) + 1;  // 32 - log2(HS)
-  for (uint32_t i = tid; i < WIN / 2; i += NT) ss.win[i] = 0;
+  for (uint32_t i = tid; i < WIN / 4; i += NT) ss.win[i] = 0;
   for (uint32_t i = tid; i < HS; i += NT) { ss.hk[i] = EMPTY; ss.hv[i] = 0; }
-  for (uint32_t i = tid; i < UnitSmem<NT, P, SM::UCAP>::NCLS; i += NT) ss.u.ccount[i] = 0;
-  if (tid == 0) { ss.u.jn[0] = ss.u.jn[1] = FULL; ss.u.lcnt = 0; }
+  if (tid == 0) ss.u.lcnt = 0;
+  cta_sync<NT>();
   uint64_t tot_acc = 0, pair_acc = 0;
+  // pipeline: cur item + slot regs, next item
+  uint32_t q = blockIdx.x;
+  uint32_t it = dealt(a, q);
+  if (it == EMPTY) return;
+  Start st = load_start<ORIENT>(a, it);
+  SlotRegs sr = load_slot<MODE>(a, st.j0 + tid, st.j1);
+  uint32_t itn = dealt(a, q + gridDim.x);
+  Start stn{};
+  if (itn != EMPTY) stn = load_start<ORIENT>(a, itn);
   for (;;) {
-    if (tid == 0) ss.u.item = atomicAdd(a.queue, 1u);
-    __syncthreads();
-    const uint32_t it = dealt(a, ss.u.item);
-    if (it == EMPTY) break;
-    const Start st = load_start<ORIENT>(a, it);
+    // prefetch: slot data of the next start, the item after it
+    SlotRegs srn{0u, 0u, 0u};
+    uint32_t itnn = EMPTY;
+    Start stnn{};
+    if (itn != EMPTY) {
+      srn = load_slot<MODE>(a, stn.j0 + tid, stn.j1);
+      itnn = dealt(a, q + 2 * gridDim.x);
+      if (itnn != EMPTY) stnn = load_start<ORIENT>(a, itnn);
+    }
+    // ---- the current start
+    units_write<NT, P, SM::UCAP>(ss.u, sr.lo, sr.len);
     uint64_t lsum = 0;
     bool hashed = false;
-    unit_start<ORIENT, MODE, NT, P, G, SM::UCAP>(a, ss.u, cs, st, CAP, ss.list, CAP, nullptr, lsum, pair_acc,
-                                                hashed);
+    start_passes<ORIENT, MODE, NT, P, G, UR, SM::UCAP>(a, ss.u, cs, st, true, 0, 0, 0, CAP, FULL, sr.len != 0,
+                                                       st.j0 + tid, sr.y, ss.list, CAP, nullptr, lsum, pair_acc,
+                                                       hashed);
     tot_acc += lsum;
     if (MODE == MODE_VERTEX) {
       const uint64_t t = warp_sum(lsum);
       if (lane == 0 && t) red_add_u64(a.bv + st.s, t);
     }
-    if (__syncthreads_or(hashed))
+    bool hz;
+    if (NT == 32) hz = __any_sync(FULL, hashed);
+    else hz = __syncthreads_or(hashed);
+    if (hz) {
       for (uint32_t i = tid; i < HS; i += NT) { ss.hk[i] = EMPTY; ss.hv[i] = 0; }
+      cta_sync<NT>();
+    }
+    if (itn == EMPTY) break;
+    q += gridDim.x;
+    st = stn;
+    sr = srn;
+    itn = itnn;
+    stn = stnn;
   }
   flush_totals(a, tot_acc, pair_acc);
 }
 
-// HEAVY tier: u32 dense window + per-CTA global overflow row; chunked.
-template <int NT, uint32_t WIN, uint32_t CAP, uint32_t LCAP, int P, int G>
+// ------------------------------------------------------------- heavy tier
+// u32 dense window + per-CTA global overflow row; chunked; dynamic queue.
+template <int NT, uint32_t WIN, uint32_t CAP, uint32_t LCAP, int P, int G, int UR>
 struct HeavySmemT {
   static constexpr uint32_t UCAP = CAP / P + NT;
-  UnitSmem<NT, P, UCAP> u;
+  Units<NT, UCAP> u;
   uint32_t win[WIN];
   uint32_t list[LCAP];
 };
 
-template <int ORIENT, int MODE, int NT, uint32_t WIN, uint32_t CAP, uint32_t LCAP, int P, int G>
+template <int ORIENT, int MODE, int NT, uint32_t WIN, uint32_t CAP, uint32_t LCAP, int P, int G, int UR>
 __global__ void __launch_bounds__(NT) k_big(CountArgs a) {
-  using SM = HeavySmemT<NT, WIN, CAP, LCAP, P, G>;
+  using SM = HeavySmemT<NT, WIN, CAP, LCAP, P, G, UR>;
   extern __shared__ __align__(16) char sm[];
   SM& hs = *(SM*)sm;
   const uint32_t tid = threadIdx.x, lane = tid & 31;
@@ -553,7 +589,6 @@ __global__ void __launch_bounds__(NT) k_big(CountArgs a) {
   uint32_t* olist = a.olist + (size_t)blockIdx.x * a.orow_len;
   const uint32_t cap = min(a.cap, CAP);
   for (uint32_t i = tid; i < WIN; i += NT) hs.win[i] = 0;
-  for (uint32_t i = tid; i < UnitSmem<NT, P, SM::UCAP>::NCLS; i += NT) hs.u.ccount[i] = 0;
   if (tid == 0) { hs.u.jn[0] = hs.u.jn[1] = FULL; hs.u.lcnt = 0; }
   uint64_t tot_acc = 0, pair_acc = 0;
   for (;;) {
@@ -562,10 +597,17 @@ __global__ void __launch_bounds__(NT) k_big(CountArgs a) {
     const uint32_t it = dealt(a, hs.u.item);
     if (it == EMPTY) break;
     const Start st = load_start<ORIENT>(a, it);
+    const uint64_t base = __ldg(a.wpre + st.j0);
+    const uint64_t w = __ldg(a.wpre + st.j1) - base;
+    const bool single = w <= cap && st.j1 - st.j0 <= (uint32_t)NT;
+    bool mine;
+    uint32_t myj, myy;
+    const uint64_t K1 = units_build<MODE, NT, P, SM::UCAP>(a, hs.u, st.j0, st.j1, base, 0, cap, 0, mine, myj, myy);
+    const uint32_t jn0 = hs.u.jn[0];
     uint64_t lsum = 0;
     bool hashed = false;
-    unit_start<ORIENT, MODE, NT, P, G, SM::UCAP>(a, hs.u, cs, st, cap, hs.list, LCAP, olist, lsum, pair_acc,
-                                                hashed);
+    start_passes<ORIENT, MODE, NT, P, G, UR, SM::UCAP>(a, hs.u, cs, st, single, base, w, K1, cap, jn0, mine, myj,
+                                                       myy, hs.list, LCAP, olist, lsum, pair_acc, hashed);
     tot_acc += lsum;
     if (MODE == MODE_VERTEX) {
       const uint64_t t = warp_sum(lsum);
@@ -575,19 +617,31 @@ __global__ void __launch_bounds__(NT) k_big(CountArgs a) {
   flush_totals(a, tot_acc, pair_acc);
 }
 
-// tier configurations
+// tier configurations <NT, WIN, HS|CAP, CAP|LCAP, P, G, UR>
 // warp tier: 1-warp CTAs, w <= 512, <= 32 slots
-#define WARP_CFG 32, 4096, 512, BF_WARP_MAX_WEDGES, 8, 4
+#define WARP_CFG 32, 8192, 512, BF_WARP_MAX_WEDGES, 8, 4, 2
 using WarpSM = SmallSmem<WARP_CFG>;
 // medium tier: 128 threads, w <= 2048, <= 128 slots
-#define MED_CFG 128, 8192, 2048, BF_MEDIUM_MAX_WEDGES, 16, 4
+#define MED_CFG 128, 16384, 2048, BF_MEDIUM_MAX_WEDGES, 16, 4, 1
 using MedSM = SmallSmem<MED_CFG>;
 // heavy tier: 256 threads, chunks of <= 8192 wedges
-#define BIG_CFG 256, 8192, 8192, 4096, 32, 4
+#define BIG_CFG 256, 8192, 8192, 4096, 32, 4, 1
 using BigSM = HeavySmemT<BIG_CFG>;
 static_assert(BF_WARP_MAX_SLOTS == 32 && BF_MEDIUM_MAX_SLOTS == 128, "tier slot bounds = CTA sizes");
 
 // ============================================================ output kernels
+// bv[side base + k] += sum over stripes of hub[stripe][side][k]
+__global__ void k_hub_reduce(const uint64_t* __restrict__ hub, uint32_t nU, uint32_t nV, uint64_t* __restrict__ bv) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < 2 * HUB_KEYS; i += gridDim.x * blockDim.x) {
+    const uint32_t side = i / HUB_KEYS, k = i % HUB_KEYS;
+    if (k >= (side ? nV : nU)) continue;
+    uint64_t v = 0;
+#pragma unroll 4
+    for (uint32_t st = 0; st < HUB_STRIPES; st++) v += hub[((size_t)st * 2 + side) * HUB_KEYS + k];
+    if (v) bv[(side ? nU : 0u) + k] += v;
+  }
+}
+
 __global__ void k_unrename(const uint64_t* __restrict__ bv, const uint32_t* __restrict__ rid_of_gid, uint32_t nU,
                            uint64_t n, uint64_t* __restrict__ out_u, uint64_t* __restrict__ out_v) {
   for (uint64_t z = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; z < n; z += (uint64_t)gridDim.x * blockDim.x) {
@@ -662,7 +716,11 @@ bf_status graph_count(bf_graph* g, int mode, uint64_t* out_a, uint64_t* out_b, u
   g->queue.ensure(64);
   uint64_t* dtot = g->total.as<uint64_t>();
   CUDA_TRY(cudaMemsetAsync(dtot, 0, 16, s));
-  if (mode == MODE_VERTEX) CUDA_TRY(cudaMemsetAsync(g->bv.p, 0, (n + 1) * 8, s));
+  if (mode == MODE_VERTEX) {
+    CUDA_TRY(cudaMemsetAsync(g->bv.p, 0, (n + 1) * 8, s));
+    g->hub.ensure((size_t)HUB_STRIPES * 2 * HUB_KEYS * 8);
+    CUDA_TRY(cudaMemsetAsync(g->hub.p, 0, (size_t)HUB_STRIPES * 2 * HUB_KEYS * 8, s));
+  }
   if (mode == MODE_EDGE) {
     g->acc.ensure(std::max<uint64_t>(S, 1) * 8);
     g->be.ensure((std::max<uint64_t>(m, 1) + 1) * 8);
@@ -686,8 +744,10 @@ bf_status graph_count(bf_graph* g, int mode, uint64_t* out_a, uint64_t* out_b, u
   a.nbr = g->nbr.as<uint32_t>();
   a.wpre = g->wpre.as<uint64_t>();
   a.seglo = g->seglo.as<uint32_t>();
+  a.seglen = g->seglen.as<uint32_t>();
   a.items = g->items.as<uint4>();
   a.bv = g->bv.as<uint64_t>();
+  a.hub = g->hub.as<uint64_t>();
   a.acc = g->acc.as<uint64_t>();
   a.total = dtot;
   a.orow = g->orow.as<uint32_t>();
@@ -722,6 +782,10 @@ bf_status graph_count(bf_graph* g, int mode, uint64_t* out_a, uint64_t* out_b, u
       else if (mode == MODE_VERTEX) launch_tiers<BF_ORIENT_HIGH, MODE_VERTEX>(g, a, tier, q, s);
       else launch_tiers<BF_ORIENT_HIGH, MODE_EDGE>(g, a, tier, q, s);
     }
+  }
+  if (mode == MODE_VERTEX) {
+    k_hub_reduce<<<16, 512, 0, s>>>(g->hub.as<uint64_t>(), g->n_u, g->n_v, g->bv.as<uint64_t>());
+    KERNEL_CHECK(g);
   }
   CUDA_TRY(cudaEventRecord(g->ev[2], s));
   // a8: outputs (total stored after the array so one allreduce covers both)
