@@ -499,7 +499,7 @@ __device__ __forceinline__ SlotRegs load_slot(const CountArgs& a, uint32_t j, ui
 }
 
 template <int ORIENT, int MODE, int NT, uint32_t WIN, uint32_t HS, uint32_t CAP, int P, int G, int UR>
-__global__ void __launch_bounds__(NT) k_small(CountArgs a) {
+__global__ void __launch_bounds__(NT, 1) k_small(CountArgs a) {
   using SM = SmallSmem<NT, WIN, HS, CAP, P, G, UR>;
   extern __shared__ __align__(16) char sm[];
   SM& ss = *(SM*)sm;
@@ -576,7 +576,7 @@ struct HeavySmemT {
 };
 
 template <int ORIENT, int MODE, int NT, uint32_t WIN, uint32_t CAP, uint32_t LCAP, int P, int G, int UR>
-__global__ void __launch_bounds__(NT) k_big(CountArgs a) {
+__global__ void __launch_bounds__(NT, 1) k_big(CountArgs a) {
   using SM = HeavySmemT<NT, WIN, CAP, LCAP, P, G, UR>;
   extern __shared__ __align__(16) char sm[];
   SM& hs = *(SM*)sm;
@@ -675,16 +675,23 @@ int occupancy(K kernel, int threads, size_t smem) {
   return b > 0 ? b : 1;
 }
 
-int heavy_grid(int sms) {
-  return sms * occupancy(k_big<BF_ORIENT_HIGH, MODE_VERTEX, BIG_CFG>, 256, sizeof(BigSM));
-}
-
 template <int ORIENT, int MODE>
 void launch_tiers(bf_graph* g, CountArgs a, const uint32_t tier[4], uint32_t* queues, cudaStream_t s) {
   const int sms = g->sms;
   if (tier[1] > tier[0]) {  // heavy
     auto k = k_big<ORIENT, MODE, BIG_CFG>;
     const int grid = sms * occupancy(k, 256, sizeof(BigSM));
+    // one overflow row + touched list per CTA of this launch, indexed by key
+    // offset (< max side size); rows stay zero between starts (owners reset
+    // them), so they are cleared once when allocated
+    const size_t rows = (size_t)grid, olen = a.orow_len;
+    if (g->orow.bytes < rows * olen * 4) {
+      g->orow.ensure(rows * olen * 4);
+      g->otouch.ensure(rows * olen * 4);
+      CUDA_TRY(cudaMemsetAsync(g->orow.p, 0, rows * olen * 4, s));
+    }
+    a.orow = g->orow.as<uint32_t>();
+    a.olist = g->otouch.as<uint32_t>();
     a.t0 = tier[0]; a.t1 = tier[1]; a.queue = queues + 0;
     k<<<grid, 256, sizeof(BigSM), s>>>(a);
     KERNEL_CHECK(g);
@@ -726,20 +733,9 @@ bf_status graph_count(bf_graph* g, int mode, uint64_t* out_a, uint64_t* out_b, u
     g->be.ensure((std::max<uint64_t>(m, 1) + 1) * 8);
     CUDA_TRY(cudaMemsetAsync(g->acc.p, 0, std::max<uint64_t>(S, 1) * 8, s));
   }
-  // heavy tier: one overflow row + touched list per resident CTA, indexed by
-  // key offset (< max side size); rows stay zero between starts (owners reset
-  // them), so they are cleared once when allocated
   const uint32_t win = (g->opt.test_flags & BF_FLAG_SMALL_WINDOW) ? 64u : 0xFFFFFFFFu;
   const uint32_t cap = (g->opt.test_flags & BF_FLAG_SMALL_CHUNK) ? 64u : 0xFFFFFFFFu;
   const uint64_t olen = std::max<uint64_t>(std::max(g->n_u, g->n_v), 1);
-  if (g->n_tier[0]) {
-    const size_t rows = (size_t)heavy_grid(g->sms);
-    if (g->orow.bytes < rows * olen * 4) {
-      g->orow.ensure(rows * olen * 4);
-      g->otouch.ensure(rows * olen * 4);
-      CUDA_TRY(cudaMemsetAsync(g->orow.p, 0, rows * olen * 4, s));
-    }
-  }
   CountArgs a;
   a.nbr = g->nbr.as<uint32_t>();
   a.wpre = g->wpre.as<uint64_t>();
