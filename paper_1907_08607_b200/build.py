@@ -30,14 +30,15 @@ def needs_build() -> bool:
     return any(os.path.getmtime(p) > t for p in deps())
 
 
-def build(force: bool = False, verbose: bool = False, debug: bool = False) -> str:
-    """debug=True builds libbf_debug.so (device bounds checks, -DBF_DEBUG); load it
-    with BF_LIB=libbf_debug.so."""
-    so = SO.replace("libbf.so", "libbf_debug.so") if debug else SO
-    if not force and not debug and not needs_build():
+def build(force: bool = False, verbose: bool = False, debug: bool = False, profile: bool = False) -> str:
+    """debug=True builds libbf_debug.so (device bounds checks, -DBF_DEBUG);
+    profile=True builds libbf_prof.so (per-phase clock64 timing, -DBF_PROFILE).
+    Load either with BF_LIB=<name>."""
+    so = SO.replace("libbf.so", "libbf_debug.so") if debug else (SO.replace("libbf.so", "libbf_prof.so") if profile else SO)
+    if not force and not debug and not profile and not needs_build():
         return SO
     cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "--shared", "-Xcompiler", "-fPIC", "-Xptxas", "-v" if verbose else "-O3",
-           *(["-DBF_DEBUG"] if debug else []),
+           *(["-DBF_DEBUG"] if debug else []), *(["-DBF_PROFILE"] if profile else []),
            "-I", os.path.join(HERE, "..", "include"), "-o", so + ".tmp", *sources(), "-ldl"]
     subprocess.check_call(cmd)
     os.replace(so + ".tmp", so)
@@ -45,4 +46,4 @@ def build(force: bool = False, verbose: bool = False, debug: bool = False) -> st
 
 
 if __name__ == "__main__":
-    print(build(force=True, verbose="-v" in sys.argv, debug="--debug" in sys.argv))
+    print(build(force=True, verbose="-v" in sys.argv, debug="--debug" in sys.argv, profile="--profile" in sys.argv))

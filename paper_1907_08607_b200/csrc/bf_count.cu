@@ -48,7 +48,9 @@
 #include "bf_device.cuh"
 #include <algorithm>
 #include <type_traits>
+#include <mutex>
 #include <stdlib.h>
+#include <stdio.h>
 
 namespace {
 
@@ -66,14 +68,17 @@ struct CountArgs {
   uint64_t* total;        // [0] total, [1] distinct pairs
   uint32_t* orow;         // heavy: per-CTA overflow rows (indexed by key offset)
   uint32_t* olist;        // heavy: per-CTA touched lists (multi-chunk starts)
-  uint64_t orow_len;
+  uint64_t orow_len;       // heavy overflow row length (max side size - heavy window)
+  uint64_t olist_len;      // heavy touched-list capacity beyond the shared list (max side size)
   uint32_t* queue;        // tier cursor
   uint32_t n_u, n_v;
   uint32_t t0, t1;        // this tier's segment of the item list
   uint64_t S, n;          // slots, vertices (bounds checks of the debug build)
   uint32_t dbg_stop;      // debug build: stop each start after this phase (0 = never)
   uint32_t exp;           // timing experiments (env BF_EXPERIMENT; results are wrong when set):
-                          // 1 = skip endpoint REDs, 2 = skip centre REDs
+                          // 1 = skip endpoint REDs, 2 = skip centre REDs, 4 = pass 1 loads
+                          // keys but skips the counters, 8 = pass 1 fakes keys without loads,
+                          // 16 = no owner lists
   uint32_t win;           // dense window keys in use (<= compile-time size)
   uint32_t cap;           // heavy chunk capacity in wedges (<= HV_CAP)
   int rank, world;
@@ -122,6 +127,37 @@ __device__ __forceinline__ void flush_totals(const CountArgs& a, uint64_t tot_ac
     if (pair_acc) red_add_u64(a.total + 1, pair_acc);
   }
 }
+
+// Phase timing of the wedge kernels (libbf_prof.so, -DBF_PROFILE): thread 0
+// of every CTA accumulates clock64() deltas per phase into g_prof, which
+// graph_count prints to stderr.  Compiles to nothing otherwise.
+#ifdef BF_PROFILE
+__device__ unsigned long long g_prof[3][8];
+__device__ unsigned long long g_prof_red[4];  // endpoint REDs: all, key < 256, < 1024, < 4096 (side-relative)
+struct Prof {
+  long long t;
+  unsigned long long acc[8];
+  __device__ __forceinline__ void start() {
+    t = clock64();
+    for (int i = 0; i < 8; i++) acc[i] = 0;
+  }
+  __device__ __forceinline__ void mark(int i) {
+    const long long n = clock64();
+    acc[i] += (unsigned long long)(n - t);
+    t = n;
+  }
+  __device__ __forceinline__ void flush(int tier) {
+    if (threadIdx.x == 0)
+      for (int i = 0; i < 8; i++) atomicAdd(&g_prof[tier][i], acc[i]);
+  }
+};
+#else
+struct Prof {
+  __device__ __forceinline__ void start() {}
+  __device__ __forceinline__ void mark(int) {}
+  __device__ __forceinline__ void flush(int) {}
+};
+#endif
 
 // Endpoint contributions C(d,2) land on the aggregated keys, which in the
 // HIGH orientation are the few highest-ranked vertices of each side: one
@@ -190,16 +226,16 @@ struct HeavyStore {
   uint32_t wl;
   uint64_t lenchk;
   __device__ __forceinline__ bool add(uint32_t, uint32_t kk, bool&) const {
-    BF_CHECK(kk < lenchk);
-    const uint32_t old = kk < wl ? atomicAdd(win + kk, 1u) : atomicAdd(orow + kk, 1u);
+    BF_CHECK(kk < wl || kk - wl < lenchk);
+    const uint32_t old = kk < wl ? atomicAdd(win + kk, 1u) : atomicAdd(orow + (kk - wl), 1u);
     return old == 0u;
   }
   __device__ __forceinline__ uint32_t get(uint32_t, uint32_t kk) const {
-    return kk < wl ? win[kk] : __ldcg(orow + kk);
+    return kk < wl ? win[kk] : __ldcg(orow + (kk - wl));
   }
   __device__ __forceinline__ void zero(uint32_t kk) const {
     if (kk < wl) win[kk] = 0;
-    else __stcg(orow + kk, 0u);
+    else __stcg(orow + (kk - wl), 0u);
   }
 };
 
@@ -214,6 +250,7 @@ template <int NT, uint32_t UCAP>
 struct Units {
   using SlotT = typename std::conditional<(NT <= 256), uint8_t, uint16_t>::type;
   uint32_t lo[UCAP];           // first nbr index of the unit
+  uint16_t pos[UCAP];          // chunk position of the unit's first wedge (key cache index)
   uint8_t len[UCAP];           // 1..P
   SlotT slot[UCAP];            // chunk-local slot (thread) of the unit
   uint32_t slo[NT], shi[NT];   // pass-2 per-slot sums (u64 as two u32)
@@ -248,14 +285,17 @@ __device__ __forceinline__ void units_write(Units<NT, UCAP>& u, uint32_t lo, uin
   constexpr uint32_t LP = 31 - __builtin_clz(P);
   const uint32_t nu = (L + P - 1) >> LP;
   uint32_t total;
-  const uint32_t ex = cta_scan<NT>(nu, u.wt, total);
-  BF_CHECK(ex + nu <= UCAP);
+  // one scan of (wedges << 16 | units): chunk wedges <= 65535, units <= 65535
+  const uint32_t pk = cta_scan<NT>((L << 16) | nu, u.wt, total);
+  const uint32_t ex = pk & 0xffffu, wp = pk >> 16;
+  BF_CHECK(ex + nu <= UCAP && L < 65536);
   for (uint32_t f = 0; f < nu; f++) {
     u.lo[ex + f] = lo + (f << LP);
+    u.pos[ex + f] = (uint16_t)(wp + (f << LP));
     u.len[ex + f] = (uint8_t)min(L - (f << LP), (uint32_t)P);
     u.slot[ex + f] = (typename Units<NT, UCAP>::SlotT)threadIdx.x;
   }
-  if (threadIdx.x == 0) u.nunits = total;
+  if (threadIdx.x == 0) u.nunits = total & 0xffffu;
   u.slo[threadIdx.x] = 0;
   u.shi[threadIdx.x] = 0;
   cta_sync<NT>();
@@ -314,22 +354,23 @@ __device__ __forceinline__ uint32_t list_get(const uint32_t* list, uint32_t lcap
 template <int NT, int P, int G, int UR, uint32_t UCAP, class Store>
 __device__ __forceinline__ void units_pass1(const CountArgs& a, Units<NT, UCAP>& u, const Store& cs,
                                             uint32_t kbase, uint32_t* list, uint32_t lcap, uint32_t* olist,
-                                            bool& hashed) {
+                                            bool& hashed, uint32_t* cache) {
   constexpr int IT = P / G;
   constexpr uint32_t NG = NT / G;
   const uint32_t tid = threadIdx.x, gl = tid & (G - 1);
   const uint32_t nunits = u.nunits;
   for (uint32_t x0 = tid / G; x0 < nunits; x0 += NG * UR) {
-    uint32_t key[UR][IT];
+    uint32_t key[UR][IT], ps[UR];
 #pragma unroll
     for (int r = 0; r < UR; r++) {
       const uint32_t x = x0 + r * NG;
       const uint32_t lo = x < nunits ? u.lo[x] : 0u, len = x < nunits ? u.len[x] : 0u;
+      ps[r] = x < nunits ? u.pos[x] : 0u;
 #pragma unroll
       for (int it = 0; it < IT; it++) {
         const uint32_t i = gl + it * G;
         BF_CHECK(i >= len || lo + i < a.S);
-        key[r][it] = i < len ? __ldg(a.nbr + (lo + i)) : EMPTY;
+        key[r][it] = i < len ? ((a.exp & 8) ? kbase + ((lo + i) & 4095u) : __ldg(a.nbr + (lo + i))) : EMPTY;
       }
     }
 #pragma unroll
@@ -339,7 +380,9 @@ __device__ __forceinline__ void units_pass1(const CountArgs& a, Units<NT, UCAP>&
         const uint32_t k = key[r][it];
         if (k != EMPTY) {
           BF_CHECK(k < a.n);
-          if (cs.add(k, k - kbase, hashed)) list_push(&u.lcnt, list, lcap, olist, a.orow_len, k);
+          if (cache) cache[ps[r] + gl + it * G] = k;
+          if (a.exp & 4) { hashed |= (k == 0xFFFFFFFEu); continue; }  // experiment: loads only
+          if (cs.add(k, k - kbase, hashed) && !(a.exp & 16)) list_push(&u.lcnt, list, lcap, olist, a.olist_len, k);
         }
       }
   }
@@ -348,35 +391,44 @@ __device__ __forceinline__ void units_pass1(const CountArgs& a, Units<NT, UCAP>&
 // pass 2 over the chunk's units: c = d(key) - 1 per wedge, summed per slot
 // (centre y in vertex mode, edge (s, y) in edge mode); edge mode also adds c
 // to the wedge's (y, key) edge
-template <int MODE, int NT, int P, int G, uint32_t UCAP, class Store>
+template <int MODE, int NT, int P, int G, int UR, uint32_t UCAP, class Store>
 __device__ __forceinline__ void units_pass2(const CountArgs& a, Units<NT, UCAP>& u, const Store& cs,
-                                            uint32_t kbase) {
+                                            uint32_t kbase, const uint32_t* cache) {
   constexpr int IT = P / G;
+  constexpr uint32_t NG = NT / G;
   const uint32_t tid = threadIdx.x, gl = tid & (G - 1);
   const uint32_t nunits = u.nunits;
   // warp-uniform trip count: the group reduction below is a full-warp shuffle
-  for (uint32_t xb = (tid & ~31u) / G; xb < nunits; xb += NT / G) {
-    const uint32_t x = xb + (tid & 31) / G;
-    const bool act = x < nunits;
-    const uint32_t lo = act ? u.lo[x] : 0u, len = act ? u.len[x] : 0u;
-    uint32_t key[IT];
+  for (uint32_t xb = (tid & ~31u) / G; xb < nunits; xb += NG * UR) {
+    uint32_t key[UR][IT], lo[UR];
 #pragma unroll
-    for (int it = 0; it < IT; it++) {
-      const uint32_t i = gl + it * G;
-      key[it] = i < len ? __ldg(a.nbr + (lo + i)) : EMPTY;
-    }
-    uint64_t s = 0;
+    for (int r = 0; r < UR; r++) {
+      const uint32_t x = xb + r * NG + (tid & 31) / G;
+      const bool act = x < nunits;
+      lo[r] = act ? u.lo[x] : 0u;
+      const uint32_t len = act ? u.len[x] : 0u, ps = act ? u.pos[x] : 0u;
 #pragma unroll
-    for (int it = 0; it < IT; it++) {
-      if (key[it] != EMPTY) {
-        const uint32_t c = cs.get(key[it], key[it] - kbase) - 1u;
-        s += c;
-        if (MODE == MODE_EDGE && c) red_add_u64(a.acc + (lo + gl + it * G), c);  // edge (y, key)
+      for (int it = 0; it < IT; it++) {
+        const uint32_t i = gl + it * G;
+        key[r][it] = i < len ? (cache ? cache[ps + i] : __ldg(a.nbr + (lo[r] + i))) : EMPTY;
       }
     }
 #pragma unroll
-    for (int o = 1; o < G; o <<= 1) s += __shfl_xor_sync(FULL, s, o);
-    if (act && gl == 0 && s) seg_add(u.slo, u.shi, u.slot[x], s);
+    for (int r = 0; r < UR; r++) {
+      const uint32_t x = xb + r * NG + (tid & 31) / G;
+      uint64_t s = 0;
+#pragma unroll
+      for (int it = 0; it < IT; it++) {
+        if (key[r][it] != EMPTY) {
+          const uint32_t c = cs.get(key[r][it], key[r][it] - kbase) - 1u;
+          s += c;
+          if (MODE == MODE_EDGE && c) red_add_u64(a.acc + (lo[r] + gl + it * G), c);  // edge (y, key)
+        }
+      }
+#pragma unroll
+      for (int o = 1; o < G; o <<= 1) s += __shfl_xor_sync(FULL, s, o);
+      if (x < nunits && gl == 0 && s) seg_add(u.slo, u.shi, u.slot[x], s);
+    }
   }
 }
 
@@ -406,6 +458,15 @@ __device__ __forceinline__ void list_finalize(const CountArgs& a, const Store& c
     const uint64_t c2 = choose2(d);
     lsum += c2;
     if (MODE == MODE_VERTEX && c2 && !(a.exp & 1)) red_add_u64(endpoint_slot(a, key), c2);
+#ifdef BF_PROFILE
+    if (c2) {
+      const uint32_t kk2 = key - (key >= a.n_u ? a.n_u : 0u);
+      atomicAdd(&g_prof_red[0], 1ull);
+      if (kk2 < 256) atomicAdd(&g_prof_red[1], 1ull);
+      if (kk2 < 1024) atomicAdd(&g_prof_red[2], 1ull);
+      if (kk2 < 4096) atomicAdd(&g_prof_red[3], 1ull);
+    }
+#endif
   }
 }
 
@@ -417,11 +478,13 @@ __device__ __forceinline__ void start_passes(const CountArgs& a, Units<NT, UCAP>
                                              const Start& st, bool single, uint64_t base, uint64_t w, uint64_t K1,
                                              uint32_t cap, uint32_t jn0, bool mine, uint32_t myj, uint32_t myy,
                                              uint32_t* list, uint32_t lcap, uint32_t* olist, uint64_t& lsum,
-                                             uint64_t& pairs, bool& hashed) {
+                                             uint64_t& pairs, bool& hashed, Prof& pf, uint32_t* cache) {
   const uint32_t tid = threadIdx.x;
   // ---- pass 1 (first chunk already built)
-  units_pass1<NT, P, G, UR, UCAP>(a, u, cs, st.kbase, list, lcap, olist, hashed);
+  units_pass1<NT, P, G, UR, UCAP>(a, u, cs, st.kbase, list, lcap, olist, hashed, single ? cache : nullptr);
+  pf.mark(2);
   cta_sync<NT>();
+  pf.mark(3);
   if (!single) {
     if (tid == 0) u.jn[0] = FULL;
     uint32_t jc = jn0 != FULL ? jn0 : ((st.j1 - st.j0 > (uint32_t)NT) ? st.j0 + NT : st.j1), par = 1;
@@ -429,7 +492,7 @@ __device__ __forceinline__ void start_passes(const CountArgs& a, Units<NT, UCAP>
     while (K0 < w) {
       const uint64_t Kn = units_build<MODE, NT, P, UCAP>(a, u, jc, st.j1, base, K0, cap, par, mine, myj, myy);
       const uint32_t jn = u.jn[par];
-      units_pass1<NT, P, G, UR, UCAP>(a, u, cs, st.kbase, list, lcap, olist, hashed);
+      units_pass1<NT, P, G, UR, UCAP>(a, u, cs, st.kbase, list, lcap, olist, hashed, nullptr);
       cta_sync<NT>();
       if (tid == 0) u.jn[par] = FULL;
       jc = jn != FULL ? jn : ((st.j1 - jc > (uint32_t)NT) ? jc + NT : st.j1);
@@ -437,14 +500,19 @@ __device__ __forceinline__ void start_passes(const CountArgs& a, Units<NT, UCAP>
       par ^= 1u;
     }
   }
+  pf.mark(1);
   const uint32_t cnt = u.lcnt;
   list_finalize<MODE, NT>(a, cs, st.kbase, cnt, list, lcap, olist, lsum);
   if (tid == 0) pairs += cnt;
+  pf.mark(4);
   if (MODE != MODE_TOTAL) {
     cta_sync<NT>();  // d is final
+    pf.mark(3);
     if (single) {
-      units_pass2<MODE, NT, P, G, UCAP>(a, u, cs, st.kbase);
+      units_pass2<MODE, NT, P, G, UR, UCAP>(a, u, cs, st.kbase, cache);
+      pf.mark(5);
       cta_sync<NT>();
+      pf.mark(3);
       slot_flush<MODE>(a, u.slo, u.shi, mine, myj, myy);
     } else {
       uint32_t jc = st.j0, par = 0;
@@ -452,7 +520,7 @@ __device__ __forceinline__ void start_passes(const CountArgs& a, Units<NT, UCAP>
       while (K0 < w) {
         const uint64_t Kn = units_build<MODE, NT, P, UCAP>(a, u, jc, st.j1, base, K0, cap, par, mine, myj, myy);
         const uint32_t jn = u.jn[par];
-        units_pass2<MODE, NT, P, G, UCAP>(a, u, cs, st.kbase);
+        units_pass2<MODE, NT, P, G, UR, UCAP>(a, u, cs, st.kbase, nullptr);
         cta_sync<NT>();
         if (tid == 0) u.jn[par] = FULL;
         slot_flush<MODE>(a, u.slo, u.shi, mine, myj, myy);
@@ -463,7 +531,9 @@ __device__ __forceinline__ void start_passes(const CountArgs& a, Units<NT, UCAP>
     }
     for (uint32_t i = tid; i < cnt; i += NT) cs.zero(list_get(list, lcap, olist, i) - st.kbase);
   }
+  pf.mark(6);
   cta_sync<NT>();
+  pf.mark(3);
   if (tid == 0) u.lcnt = 0;
 }
 
@@ -480,7 +550,8 @@ struct SmallSmem {
   uint32_t win[WIN / 4];
   uint32_t hk[HS];
   uint32_t hv[HS];
-  uint32_t list[CAP];  // distinct keys <= w <= CAP
+  uint32_t list[CAP];   // distinct keys <= w <= CAP
+  uint32_t cache[CAP];  // the start's keys in wedge order (pass 2 reads them here)
 };
 
 struct SlotRegs {
@@ -517,6 +588,8 @@ __global__ void __launch_bounds__(NT, 1) k_small(CountArgs a) {
   if (tid == 0) ss.u.lcnt = 0;
   cta_sync<NT>();
   uint64_t tot_acc = 0, pair_acc = 0;
+  Prof pf;
+  pf.start();
   // pipeline: cur item + slot regs, next item
   uint32_t q = blockIdx.x;
   uint32_t it = dealt(a, q);
@@ -536,13 +609,15 @@ __global__ void __launch_bounds__(NT, 1) k_small(CountArgs a) {
       itnn = dealt(a, q + 2 * gridDim.x);
       if (itnn != EMPTY) stnn = load_start<ORIENT>(a, itnn);
     }
+    pf.mark(0);
     // ---- the current start
     units_write<NT, P, SM::UCAP>(ss.u, sr.lo, sr.len);
+    pf.mark(1);
     uint64_t lsum = 0;
     bool hashed = false;
     start_passes<ORIENT, MODE, NT, P, G, UR, SM::UCAP>(a, ss.u, cs, st, true, 0, 0, 0, CAP, FULL, sr.len != 0,
                                                        st.j0 + tid, sr.y, ss.list, CAP, nullptr, lsum, pair_acc,
-                                                       hashed);
+                                                       hashed, pf, ss.cache);
     tot_acc += lsum;
     if (MODE == MODE_VERTEX) {
       const uint64_t t = warp_sum(lsum);
@@ -555,6 +630,7 @@ __global__ void __launch_bounds__(NT, 1) k_small(CountArgs a) {
       for (uint32_t i = tid; i < HS; i += NT) { ss.hk[i] = EMPTY; ss.hv[i] = 0; }
       cta_sync<NT>();
     }
+    pf.mark(7);
     if (itn == EMPTY) break;
     q += gridDim.x;
     st = stn;
@@ -562,6 +638,7 @@ __global__ void __launch_bounds__(NT, 1) k_small(CountArgs a) {
     itn = itnn;
     stn = stnn;
   }
+  pf.flush(NT == 32 ? 2 : 1);
   flush_totals(a, tot_acc, pair_acc);
 }
 
@@ -586,11 +663,13 @@ __global__ void __launch_bounds__(NT, 1) k_big(CountArgs a) {
   cs.orow = a.orow + (size_t)blockIdx.x * a.orow_len;
   cs.wl = min(a.win, WIN);
   cs.lenchk = a.orow_len;
-  uint32_t* olist = a.olist + (size_t)blockIdx.x * a.orow_len;
+  uint32_t* olist = a.olist + (size_t)blockIdx.x * a.olist_len;
   const uint32_t cap = min(a.cap, CAP);
   for (uint32_t i = tid; i < WIN; i += NT) hs.win[i] = 0;
   if (tid == 0) { hs.u.jn[0] = hs.u.jn[1] = FULL; hs.u.lcnt = 0; }
   uint64_t tot_acc = 0, pair_acc = 0;
+  Prof pf;
+  pf.start();
   for (;;) {
     if (tid == 0) hs.u.item = atomicAdd(a.queue, 1u);
     __syncthreads();
@@ -602,18 +681,22 @@ __global__ void __launch_bounds__(NT, 1) k_big(CountArgs a) {
     const bool single = w <= cap && st.j1 - st.j0 <= (uint32_t)NT;
     bool mine;
     uint32_t myj, myy;
+    pf.mark(0);
     const uint64_t K1 = units_build<MODE, NT, P, SM::UCAP>(a, hs.u, st.j0, st.j1, base, 0, cap, 0, mine, myj, myy);
     const uint32_t jn0 = hs.u.jn[0];
     uint64_t lsum = 0;
     bool hashed = false;
     start_passes<ORIENT, MODE, NT, P, G, UR, SM::UCAP>(a, hs.u, cs, st, single, base, w, K1, cap, jn0, mine, myj,
-                                                       myy, hs.list, LCAP, olist, lsum, pair_acc, hashed);
+                                                       myy, hs.list, LCAP, olist, lsum, pair_acc, hashed, pf,
+                                                       (uint32_t*)nullptr);
     tot_acc += lsum;
     if (MODE == MODE_VERTEX) {
       const uint64_t t = warp_sum(lsum);
       if (lane == 0 && t) red_add_u64(a.bv + st.s, t);
     }
+    pf.mark(7);
   }
+  pf.flush(0);
   flush_totals(a, tot_acc, pair_acc);
 }
 
@@ -622,10 +705,11 @@ __global__ void __launch_bounds__(NT, 1) k_big(CountArgs a) {
 #define WARP_CFG 32, 8192, 512, BF_WARP_MAX_WEDGES, 8, 4, 2
 using WarpSM = SmallSmem<WARP_CFG>;
 // medium tier: 128 threads, w <= 2048, <= 128 slots
-#define MED_CFG 128, 16384, 2048, BF_MEDIUM_MAX_WEDGES, 16, 4, 1
+#define MED_CFG 128, 16384, 2048, BF_MEDIUM_MAX_WEDGES, 16, 4, 2
 using MedSM = SmallSmem<MED_CFG>;
 // heavy tier: 256 threads, chunks of <= 8192 wedges
 #define BIG_CFG 256, 8192, 8192, 4096, 32, 4, 1
+constexpr uint64_t HV_WIN_KEYS = 8192;  // BIG_CFG's window
 using BigSM = HeavySmemT<BIG_CFG>;
 static_assert(BF_WARP_MAX_SLOTS == 32 && BF_MEDIUM_MAX_SLOTS == 128, "tier slot bounds = CTA sizes");
 
@@ -675,23 +759,45 @@ int occupancy(K kernel, int threads, size_t smem) {
   return b > 0 ? b : 1;
 }
 
+// Per-device pool of heavy-tier overflow rows + touched lists.  The lock is
+// held by graph_count for the whole call; a failed call marks the rows dirty.
+struct RowPool {
+  std::mutex m;
+  void* p = nullptr;
+  size_t bytes = 0;
+  bool dirty = false;
+};
+constexpr size_t kRowPoolBudget = (size_t)16 << 30;
+RowPool& row_pool(int dev) {
+  static RowPool pools[64];
+  return pools[dev & 63];
+}
+
 template <int ORIENT, int MODE>
 void launch_tiers(bf_graph* g, CountArgs a, const uint32_t tier[4], uint32_t* queues, cudaStream_t s) {
   const int sms = g->sms;
   if (tier[1] > tier[0]) {  // heavy
     auto k = k_big<ORIENT, MODE, BIG_CFG>;
-    const int grid = sms * occupancy(k, 256, sizeof(BigSM));
-    // one overflow row + touched list per CTA of this launch, indexed by key
-    // offset (< max side size); rows stay zero between starts (owners reset
-    // them), so they are cleared once when allocated
-    const size_t rows = (size_t)grid, olen = a.orow_len;
-    if (g->orow.bytes < rows * olen * 4) {
-      g->orow.ensure(rows * olen * 4);
-      g->otouch.ensure(rows * olen * 4);
-      CUDA_TRY(cudaMemsetAsync(g->orow.p, 0, rows * olen * 4, s));
+    int grid = sms * occupancy(k, 256, sizeof(BigSM));
+    // one overflow row + touched list per CTA, from the device's row pool
+    // (rows are kept zero by the owners' resets, so a clean pool is reused
+    // across graphs without clearing); the grid shrinks if the rows of every
+    // CTA would exceed the pool budget
+    const size_t row_bytes = (a.orow_len + a.olist_len) * 4;
+    grid = (int)std::max<size_t>(1, std::min<size_t>((size_t)grid, kRowPoolBudget / row_bytes));
+    RowPool& pool = row_pool(g->device);
+    const size_t need = (size_t)grid * row_bytes;
+    if (pool.bytes < need || pool.dirty) {
+      if (pool.p) CUDA_TRY(cudaFree(pool.p));
+      pool.p = nullptr;
+      pool.bytes = 0;
+      CUDA_TRY(cudaMalloc(&pool.p, need));
+      pool.bytes = need;
+      CUDA_TRY(cudaMemsetAsync(pool.p, 0, need, s));
+      pool.dirty = false;
     }
-    a.orow = g->orow.as<uint32_t>();
-    a.olist = g->otouch.as<uint32_t>();
+    a.orow = (uint32_t*)pool.p;                                  // [grid][orow_len]
+    a.olist = (uint32_t*)pool.p + (size_t)grid * a.orow_len;     // [grid][olist_len]
     a.t0 = tier[0]; a.t1 = tier[1]; a.queue = queues + 0;
     k<<<grid, 256, sizeof(BigSM), s>>>(a);
     KERNEL_CHECK(g);
@@ -736,6 +842,17 @@ bf_status graph_count(bf_graph* g, int mode, uint64_t* out_a, uint64_t* out_b, u
   const uint32_t win = (g->opt.test_flags & BF_FLAG_SMALL_WINDOW) ? 64u : 0xFFFFFFFFu;
   const uint32_t cap = (g->opt.test_flags & BF_FLAG_SMALL_CHUNK) ? 64u : 0xFFFFFFFFu;
   const uint64_t olen = std::max<uint64_t>(std::max(g->n_u, g->n_v), 1);
+  // the heavy tier's row pool is held for the whole call (rows must be clean
+  // when the next call on this device starts)
+  std::unique_lock<std::mutex> pool_lock;
+  struct DirtyGuard {
+    RowPool* p = nullptr;
+    ~DirtyGuard() { if (p) p->dirty = true; }
+  } dirty_guard;
+  if (g->n_tier[0]) {
+    pool_lock = std::unique_lock<std::mutex>(row_pool(g->device).m);
+    dirty_guard.p = &row_pool(g->device);
+  }
   CountArgs a;
   a.nbr = g->nbr.as<uint32_t>();
   a.wpre = g->wpre.as<uint64_t>();
@@ -746,9 +863,11 @@ bf_status graph_count(bf_graph* g, int mode, uint64_t* out_a, uint64_t* out_b, u
   a.hub = g->hub.as<uint64_t>();
   a.acc = g->acc.as<uint64_t>();
   a.total = dtot;
-  a.orow = g->orow.as<uint32_t>();
-  a.olist = g->otouch.as<uint32_t>();
-  a.orow_len = olen;
+  a.orow = nullptr;
+  a.olist = nullptr;
+  const uint64_t hwl = std::min<uint64_t>(win, HV_WIN_KEYS);  // the heavy kernel's window in keys
+  a.orow_len = olen > hwl ? olen - hwl : 1;
+  a.olist_len = olen;
   a.S = S;
   a.n = n;
   a.exp = getenv("BF_EXPERIMENT") ? (uint32_t)atoi(getenv("BF_EXPERIMENT")) : 0u;
@@ -763,6 +882,13 @@ bf_status graph_count(bf_graph* g, int mode, uint64_t* out_a, uint64_t* out_b, u
   const int G = g->opt.world_size > 1 ? g->opt.world_size : V;
   const int first = g->opt.world_size > 1 ? g->opt.world_rank : 0;
   const int last = g->opt.world_size > 1 ? g->opt.world_rank : V - 1;
+#ifdef BF_PROFILE
+  {
+    unsigned long long z[24] = {0};
+    CUDA_TRY(cudaMemcpyToSymbolAsync(g_prof, z, sizeof(z), 0, cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemcpyToSymbolAsync(g_prof_red, z, 32, 0, cudaMemcpyHostToDevice, s));
+  }
+#endif
   CUDA_TRY(cudaEventRecord(g->ev[1], s));
   for (int r = first; r <= last; r++) {
     a.rank = r;
@@ -784,6 +910,27 @@ bf_status graph_count(bf_graph* g, int mode, uint64_t* out_a, uint64_t* out_b, u
     KERNEL_CHECK(g);
   }
   CUDA_TRY(cudaEventRecord(g->ev[2], s));
+#ifdef BF_PROFILE
+  {
+    unsigned long long h[24];
+    CUDA_TRY(cudaMemcpyFromSymbolAsync(h, g_prof, sizeof(h), 0, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    unsigned long long hr[4];
+    CUDA_TRY(cudaMemcpyFromSymbolAsync(hr, g_prof_red, 32, 0, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    fprintf(stderr, "[bf_prof] endpoint REDs %llu (key<256 %llu, <1024 %llu, <4096 %llu)\n", hr[0], hr[1], hr[2], hr[3]);
+    const char* names[8] = {"fetch", "build", "pass1", "sync", "final", "pass2", "flush", "tail"};
+    const char* tiers[3] = {"heavy", "medium", "warp"};
+    for (int t = 0; t < 3; t++) {
+      unsigned long long tot = 0;
+      for (int i = 0; i < 8; i++) tot += h[t * 8 + i];
+      if (!tot) continue;
+      fprintf(stderr, "[bf_prof] %-6s", tiers[t]);
+      for (int i = 0; i < 8; i++) fprintf(stderr, " %s=%.1f%%", names[i], 100.0 * h[t * 8 + i] / tot);
+      fprintf(stderr, " (cta-cycles %.3g)\n", (double)tot);
+    }
+  }
+#endif
   // a8: outputs (total stored after the array so one allreduce covers both)
   uint64_t* red_buf = nullptr;
   size_t red_cnt = 0;
@@ -839,6 +986,7 @@ bf_status graph_count(bf_graph* g, int mode, uint64_t* out_a, uint64_t* out_b, u
   CUDA_TRY(cudaEventRecord(g->ev[3], s));
   CUDA_TRY(cudaStreamSynchronize(s));
   g->last_pairs = hpairs;
+  dirty_guard.p = nullptr;  // completed: rows are clean again
   CUDA_TRY(cudaEventElapsedTime(&g->last_kernel_ms, g->ev[1], g->ev[2]));
   CUDA_TRY(cudaEventElapsedTime(&g->last_call_ms, g->ev[0], g->ev[3]));
   return BF_OK;

@@ -7,3 +7,4 @@ import json; d=json.loads(open('gpurun_out/${tag}_$mode.json').readline())
 print('$mode kernel_ms %.3f step_ms %.3f' % (d['count_only']['kernel_ms'], d['ms_per_step']))"
 done
 timeout 200 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${tag}_launches.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > /dev/null 2>&1; python tools/launch_summary.py gpurun_out/${tag}_launches.csv | head -8
+BF_LIB=libbf_prof.so timeout 100 python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e 2>&1 | grep "bf_prof" | tail -4
