@@ -69,8 +69,9 @@ typedef enum { BF_ORIENT_AUTO = 0, BF_ORIENT_LOW = 1, BF_ORIENT_HIGH = 2 } bf_or
 /* test_flags bits (path forcing for tests; 0 in production).  Tiers of the
  * work plan: warp tier (w <= 512 wedges and <= 32 slots; per-warp u16 dense
  * key window + overflow hash), CTA medium tier (w <= 2048) and CTA heavy tier
- * (dense shared-memory key window + per-CTA global overflow row).  Results
- * never depend on these flags. */
+ * (dense shared-memory key window + per-CTA global overflow row); heavy starts
+ * above max(2^20, W / (8 * #SMs)) wedges are split into pieces counted by many
+ * CTAs into one global d-row.  Results never depend on these flags. */
 #define BF_FLAG_FORCE_WARP      0x1u  /* no medium tier: warp tier for every start it
                                          can hold, heavy CTA tier for the rest          */
 #define BF_FLAG_FORCE_CTA       0x2u  /* no warp tier: CTA medium / heavy tiers only    */
@@ -80,7 +81,9 @@ typedef enum { BF_ORIENT_AUTO = 0, BF_ORIENT_LOW = 1, BF_ORIENT_HIGH = 2 } bf_or
 #define BF_FLAG_CHECK_OVERFLOW  0x8u  /* reserved                                      */
 #define BF_FLAG_FORCE_DENSE     0x10u /* every start on the heavy CTA tier             */
 #define BF_FLAG_SMALL_CHUNK     0x20u /* CTA chunks of 64 wedges: every CTA start with
-                                         more wedges takes the multi-chunk path         */
+                                         more wedges takes the multi-chunk path; the
+                                         split threshold drops to 256 wedges            */
+#define BF_FLAG_NO_SPLIT        0x40u /* never split a start across CTAs                */
 
 typedef struct {
   int device;               /* CUDA ordinal                                           */

@@ -228,6 +228,31 @@ __global__ void k_order_keys(const uint64_t* __restrict__ wstart, const uint32_t
   }
 }
 
+// piece k of split start i covers slots [b_k, b_{k+1}) with b_k = the first
+// slot whose wedge prefix reaches k/n of the start's wedges (binary search)
+__global__ void k_pieces(const uint4* __restrict__ split, const uint4* __restrict__ pdesc, uint32_t np,
+                         const uint64_t* __restrict__ wpre, uint4* __restrict__ pieces) {
+  for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < np; p += gridDim.x * blockDim.x) {
+    const uint4 d = pdesc[p];  // {split index, k, n, -}
+    const uint4 sp = split[d.x];
+    const uint64_t base = wpre[sp.y], w = wpre[sp.z] - base;
+    uint32_t b[2];
+    for (int e = 0; e < 2; e++) {
+      const uint32_t k = d.y + e;
+      if (k == 0) { b[e] = sp.y; continue; }
+      if (k == d.z) { b[e] = sp.z; continue; }
+      const uint64_t target = base + (uint64_t)((unsigned __int128)w * k / d.z);
+      uint32_t lo = sp.y, hi = sp.z;  // first j in [lo, hi] with wpre[j] >= target
+      while (lo < hi) {
+        const uint32_t mid = lo + (hi - lo) / 2;
+        if (wpre[mid] >= target) hi = mid; else lo = mid + 1;
+      }
+      b[e] = lo;
+    }
+    pieces[p] = make_uint4(d.x, b[0], b[1], 0u);
+  }
+}
+
 __global__ void k_compact2(const uint32_t* __restrict__ flag, const uint32_t* __restrict__ idx,
                            const uint32_t* __restrict__ key, uint64_t n, uint32_t* __restrict__ out_rid,
                            uint32_t* __restrict__ out_key) {
@@ -236,6 +261,8 @@ __global__ void k_compact2(const uint32_t* __restrict__ flag, const uint32_t* __
 }
 
 }  // namespace
+
+static bf_status plan_split(bf_graph* g);
 
 bf_status graph_ingest(bf_graph* g, const uint32_t* edges) {
   cudaStream_t s = g->stream;
@@ -428,5 +455,74 @@ bf_status graph_plan(bf_graph* g) {
                                                    g->items.as<uint4>());
     KERNEL_CHECK(g);
   }
+  return plan_split(g);
+}
+
+// Split starts: heavy starts whose wedges exceed the threshold (a share of W
+// that one CTA would take much longer than the rest of the kernel to finish)
+// are cut into pieces of about threshold/2 wedges.  The heavy tier's items are
+// sorted by wedges, so the split starts are its prefix.
+static bf_status plan_split(bf_graph* g) {
+  cudaStream_t s = g->stream;
+  g->n_split = 0;
+  g->split_batches.clear();
+  const uint64_t tmin = (g->opt.test_flags & BF_FLAG_SMALL_CHUNK) ? 256u : ((uint64_t)1 << 20);
+  g->split_threshold = std::max<uint64_t>(tmin, g->W / ((uint64_t)g->sms * 8));
+  if (g->opt.test_flags & BF_FLAG_NO_SPLIT) g->split_threshold = ~0ull;
+  const uint32_t nh = std::min<uint32_t>(g->n_tier[0], kMaxSplit);
+  if (!nh) return BF_OK;
+  std::vector<uint4> it(nh);
+  CUDA_TRY(cudaMemcpyAsync(it.data(), g->items.p, (size_t)nh * 16, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  uint32_t ns = 0;
+  while (ns < nh && it[ns].w > g->split_threshold) ns++;
+  if (!ns) return BF_OK;
+  // key range of each split start (HIGH: same-side rids ranked above s; LOW:
+  // ranked below), row offsets, pieces, memory-bounded batches
+  std::vector<uint64_t> off(ns);
+  std::vector<uint4> pdesc;
+  const uint64_t piece = std::max<uint64_t>(g->split_threshold / 2, 1);
+  const uint64_t budget = kSplitRowBudget / 8;  // keys: row + list, 4 B each
+  g->split_batches.push_back({0, 0, 0, 0, 0});
+  for (uint32_t i = 0; i < ns; i++) {
+    const uint32_t sv = it[i].x;
+    const bool isU = sv < g->n_u;
+    const uint64_t kr = g->orient == BF_ORIENT_HIGH ? (isU ? sv : sv - g->n_u)
+                                                    : (isU ? g->n_u - sv - 1 : g->n - sv - 1);
+    const uint64_t keys = std::max<uint64_t>(kr, 1);
+    auto* b = &g->split_batches.back();
+    if (b->s1 > b->s0 && b->keys + keys > budget) {
+      g->split_batches.push_back({i, i, (uint32_t)pdesc.size(), (uint32_t)pdesc.size(), 0});
+      b = &g->split_batches.back();
+    }
+    off[i] = b->keys;
+    b->keys += keys;
+    b->s1 = i + 1;
+    const uint32_t np = (uint32_t)std::min<uint64_t>((it[i].w + piece - 1) / piece, it[i].z - it[i].y);
+    for (uint32_t k = 0; k < std::max<uint32_t>(np, 1); k++) pdesc.push_back(make_uint4(i, k, std::max<uint32_t>(np, 1), 0));
+    b->p1 = (uint32_t)pdesc.size();
+  }
+  g->n_split = ns;
+  uint64_t maxkeys = 0;
+  for (auto& b : g->split_batches) maxkeys = std::max(maxkeys, b.keys);
+  const uint32_t npc = (uint32_t)pdesc.size();
+  g->split.ensure((size_t)ns * 16);
+  g->split_off.ensure((size_t)ns * 8);
+  g->split_cnt.ensure((size_t)ns * 4);
+  g->pieces.ensure((size_t)npc * 16);
+  g->tmp_a.ensure((size_t)npc * 16 + 64);
+  CUDA_TRY(cudaMemcpyAsync(g->split.p, it.data(), (size_t)ns * 16, cudaMemcpyHostToDevice, s));
+  CUDA_TRY(cudaMemcpyAsync(g->split_off.p, off.data(), (size_t)ns * 8, cudaMemcpyHostToDevice, s));
+  CUDA_TRY(cudaMemsetAsync(g->split_cnt.p, 0, (size_t)ns * 4, s));
+  CUDA_TRY(cudaMemcpyAsync(g->tmp_a.p, pdesc.data(), (size_t)npc * 16, cudaMemcpyHostToDevice, s));
+  k_pieces<<<grid_for(npc, g->sms), TPB, 0, s>>>(g->split.as<uint4>(), g->tmp_a.as<uint4>(), npc,
+                                                  g->wpre.as<uint64_t>(), g->pieces.as<uint4>());
+  KERNEL_CHECK(g);
+  if (g->srow.bytes < maxkeys * 4) {
+    g->srow.ensure(maxkeys * 4);
+    g->slist.ensure(maxkeys * 4);
+    CUDA_TRY(cudaMemsetAsync(g->srow.p, 0, maxkeys * 4, s));
+  }
+  CUDA_TRY(cudaStreamSynchronize(s));  // host vectors go out of scope
   return BF_OK;
 }

@@ -700,6 +700,171 @@ __global__ void __launch_bounds__(NT, 1) k_big(CountArgs a) {
   flush_totals(a, tot_acc, pair_acc);
 }
 
+// ------------------------------------------------------------- split starts
+// A start with more wedges than the split threshold is cut into pieces (slot
+// ranges of about equal wedge count) that many CTAs count at once: window keys
+// in shared memory, flushed per piece into the start's global dense d-row;
+// other keys straight into the row.  A separate finalize runs once every piece
+// is counted (the two-pass discipline), then pass 2 re-walks the
+// pieces with the row frozen.  Whole split starts are dealt to ranks.
+struct SplitArgs {
+  const uint4* split;     // {s, j0, j1, -}
+  const uint64_t* off;    // row / list offset of each split start (keys)
+  uint32_t* cnt;          // touched-list count per split start
+  const uint4* pieces;    // {split index, slot begin, slot end, -}
+  uint32_t* rows;         // dense d-rows of this batch
+  uint32_t* lists;        // touched lists of this batch
+  uint32_t s0, s1, p0, p1;
+};
+
+__device__ __forceinline__ bool split_mine(const CountArgs& a, uint32_t i) {
+  const uint32_t G = (uint32_t)a.world, q = i / G, r = i % G;
+  return (uint32_t)a.rank == ((q & 1u) ? G - 1 - r : r);
+}
+
+template <int ORIENT>
+__device__ __forceinline__ uint32_t split_kbase(const CountArgs& a, uint32_t s) {
+  return ORIENT == BF_ORIENT_HIGH ? (s < a.n_u ? 0u : a.n_u) : s + 1u;
+}
+
+struct SplitStore1 {
+  uint32_t* win;
+  uint32_t wl;
+  uint32_t* row;
+  uint32_t* glist;
+  uint32_t* gcnt;
+  __device__ __forceinline__ bool add(uint32_t key, uint32_t kk, bool&) const {
+    if (kk < wl) return atomicAdd(win + kk, 1u) == 0u;
+    if (atomicAdd(row + kk, 1u) == 0u) glist[atomicAdd(gcnt, 1u)] = key;
+    return false;
+  }
+};
+struct SplitStore2 {
+  const uint32_t* row;
+  __device__ __forceinline__ uint32_t get(uint32_t, uint32_t kk) const { return __ldcg(row + kk); }
+};
+
+constexpr int SP_NT = 256;
+constexpr uint32_t SP_WIN = 8192, SP_CAP = 8192;
+constexpr int SP_P = 32, SP_G = 4;
+struct SplitSmem {
+  static constexpr uint32_t UCAP = SP_CAP / SP_P + SP_NT;
+  Units<SP_NT, UCAP> u;
+  uint32_t win[SP_WIN];
+  uint32_t list[SP_WIN];  // window owners of the piece (distinct window keys <= SP_WIN)
+};
+
+template <int ORIENT, int MODE, bool PASS2>
+__global__ void __launch_bounds__(SP_NT, 1) k_split_walk(CountArgs a, SplitArgs sa) {
+  extern __shared__ __align__(16) char sm[];
+  SplitSmem& ss = *(SplitSmem*)sm;
+  using U = Units<SP_NT, SplitSmem::UCAP>;
+  const uint32_t tid = threadIdx.x;
+  const uint32_t cap = min(a.cap, SP_CAP);
+  if (!PASS2)
+    for (uint32_t i = tid; i < SP_WIN; i += SP_NT) ss.win[i] = 0;
+  if (tid == 0) { ss.u.jn[0] = ss.u.jn[1] = FULL; ss.u.lcnt = 0; }
+  for (;;) {
+    if (tid == 0) ss.u.item = sa.p0 + atomicAdd(a.queue, 1u);
+    __syncthreads();
+    const uint32_t p = ss.u.item;
+    __syncthreads();  // every thread has read the item before thread 0 takes the next
+    if (p >= sa.p1) break;
+    const uint4 pc = __ldg(sa.pieces + p);
+    if (!split_mine(a, pc.x)) continue;  // CTA-uniform
+    const uint4 sp = __ldg(sa.split + pc.x);
+    const uint32_t kbase = split_kbase<ORIENT>(a, sp.x);
+    uint32_t* row = sa.rows + __ldg(sa.off + pc.x);
+    uint32_t* glist = sa.lists + __ldg(sa.off + pc.x);
+    SplitStore1 s1{ss.win, min(a.win, SP_WIN), row, glist, sa.cnt + pc.x};
+    SplitStore2 s2{row};
+    const uint64_t base = __ldg(a.wpre + pc.y), w = __ldg(a.wpre + pc.z) - base;
+    uint32_t jc = pc.y, par = 0;
+    uint64_t K0 = 0;
+    bool hashed = false;
+    while (K0 < w) {
+      bool mine;
+      uint32_t myj, myy;
+      const uint64_t K1 = units_build<PASS2 ? MODE : MODE_TOTAL, SP_NT, SP_P, SplitSmem::UCAP>(
+          a, ss.u, jc, pc.z, base, K0, cap, par, mine, myj, myy);
+      const uint32_t jn = ss.u.jn[par];
+      if (PASS2) units_pass2<MODE, SP_NT, SP_P, SP_G, 1, SplitSmem::UCAP>(a, ss.u, s2, kbase, nullptr);
+      else units_pass1<SP_NT, SP_P, SP_G, 1, SplitSmem::UCAP>(a, ss.u, s1, kbase, ss.list, SP_WIN, nullptr, hashed,
+                                                              nullptr);
+      __syncthreads();
+      if (tid == 0) ss.u.jn[par] = FULL;
+      if (PASS2) slot_flush<MODE>(a, ss.u.slo, ss.u.shi, mine, myj, myy);
+      jc = jn != FULL ? jn : ((pc.z - jc > (uint32_t)SP_NT) ? jc + SP_NT : pc.z);
+      K0 = K1;
+      par ^= 1u;
+    }
+    if (!PASS2) {  // flush the piece's window counts into the start's row
+      const uint32_t cnt = ss.u.lcnt;
+      for (uint32_t i = tid; i < cnt; i += SP_NT) {
+        const uint32_t key = ss.list[i], kk = key - kbase;
+        const uint32_t c = ss.win[kk];
+        ss.win[kk] = 0;
+        if (atomicAdd(row + kk, c) == 0u) glist[atomicAdd(sa.cnt + pc.x, 1u)] = key;
+      }
+      __syncthreads();
+      if (tid == 0) ss.u.lcnt = 0;
+    }
+  }
+}
+
+// finalize (after every piece is counted): C(d,2) to the total and both
+// endpoints; total mode also resets the row and the list here
+template <int ORIENT, int MODE>
+__global__ void __launch_bounds__(256) k_split_finalize(CountArgs a, SplitArgs sa) {
+  uint64_t tot_acc = 0, pair_acc = 0;
+  __shared__ unsigned long long s_sum;
+  for (uint32_t i = sa.s0 + blockIdx.x; i < sa.s1; i += gridDim.x) {
+    if (!split_mine(a, i)) continue;
+    const uint4 sp = __ldg(sa.split + i);
+    const uint32_t kbase = split_kbase<ORIENT>(a, sp.x);
+    uint32_t* row = sa.rows + sa.off[i];
+    const uint32_t* glist = sa.lists + sa.off[i];
+    const uint32_t cnt = __ldcg(sa.cnt + i);
+    if (threadIdx.x == 0) s_sum = 0;
+    __syncthreads();
+    uint64_t lsum = 0;
+    for (uint32_t t = threadIdx.x; t < cnt; t += blockDim.x) {
+      const uint32_t key = __ldcg(glist + t), kk = key - kbase;
+      const uint32_t d = __ldcg(row + kk);
+      if (MODE == MODE_TOTAL) __stcg(row + kk, 0u);
+      const uint64_t c2 = choose2(d);
+      lsum += c2;
+      if (MODE == MODE_VERTEX && c2) red_add_u64(endpoint_slot(a, key), c2);
+    }
+    tot_acc += lsum;
+    if (threadIdx.x == 0) pair_acc += cnt;
+    if (MODE == MODE_VERTEX) {
+      const uint64_t t = warp_sum(lsum);
+      if ((threadIdx.x & 31) == 0 && t) atomicAdd(&s_sum, (unsigned long long)t);
+      __syncthreads();
+      if (threadIdx.x == 0 && s_sum) red_add_u64(a.bv + sp.x, s_sum);
+    }
+    __syncthreads();
+    if (MODE == MODE_TOTAL && threadIdx.x == 0) sa.cnt[i] = 0;
+  }
+  flush_totals(a, tot_acc, pair_acc);
+}
+
+// reset rows and lists after pass 2
+template <int ORIENT>
+__global__ void __launch_bounds__(256) k_split_clear(CountArgs a, SplitArgs sa) {
+  for (uint32_t i = sa.s0 + blockIdx.x; i < sa.s1; i += gridDim.x) {
+    if (!split_mine(a, i)) continue;
+    const uint32_t kbase = split_kbase<ORIENT>(a, __ldg(sa.split + i).x);
+    uint32_t* row = sa.rows + sa.off[i];
+    const uint32_t* glist = sa.lists + sa.off[i];
+    const uint32_t cnt = __ldcg(sa.cnt + i);
+    for (uint32_t t = threadIdx.x; t < cnt; t += blockDim.x) __stcg(row + (__ldcg(glist + t) - kbase), 0u);
+    __syncthreads();
+    if (threadIdx.x == 0) sa.cnt[i] = 0;
+  }
+}
+
 // tier configurations <NT, WIN, HS|CAP, CAP|LCAP, P, G, UR>
 // warp tier: 1-warp CTAs, w <= 512, <= 32 slots
 #define WARP_CFG 32, 8192, 512, BF_WARP_MAX_WEDGES, 8, 4, 2
@@ -776,7 +941,36 @@ RowPool& row_pool(int dev) {
 template <int ORIENT, int MODE>
 void launch_tiers(bf_graph* g, CountArgs a, const uint32_t tier[4], uint32_t* queues, cudaStream_t s) {
   const int sms = g->sms;
-  if (tier[1] > tier[0]) {  // heavy
+  if (g->n_split) {  // split starts, batch by batch
+    for (const auto& b : g->split_batches) {
+      SplitArgs sa;
+      sa.split = g->split.as<uint4>();
+      sa.off = g->split_off.as<uint64_t>();
+      sa.cnt = g->split_cnt.as<uint32_t>();
+      sa.pieces = g->pieces.as<uint4>();
+      sa.rows = g->srow.as<uint32_t>();
+      sa.lists = g->slist.as<uint32_t>();
+      sa.s0 = b.s0; sa.s1 = b.s1; sa.p0 = b.p0; sa.p1 = b.p1;
+      auto k1 = k_split_walk<ORIENT, MODE, false>;
+      const int grid = sms * occupancy(k1, SP_NT, sizeof(SplitSmem));
+      const int fgrid = (int)std::min<uint32_t>(b.s1 - b.s0, (uint32_t)sms * 8);
+      CUDA_TRY(cudaMemsetAsync(queues + 4, 0, 8, s));
+      a.queue = queues + 4;
+      k1<<<grid, SP_NT, sizeof(SplitSmem), s>>>(a, sa);
+      KERNEL_CHECK(g);
+      k_split_finalize<ORIENT, MODE><<<fgrid, 256, 0, s>>>(a, sa);
+      KERNEL_CHECK(g);
+      if (MODE != MODE_TOTAL) {
+        auto k2 = k_split_walk<ORIENT, MODE, true>;
+        a.queue = queues + 5;
+        k2<<<sms * occupancy(k2, SP_NT, sizeof(SplitSmem)), SP_NT, sizeof(SplitSmem), s>>>(a, sa);
+        KERNEL_CHECK(g);
+        k_split_clear<ORIENT><<<fgrid, 256, 0, s>>>(a, sa);
+        KERNEL_CHECK(g);
+      }
+    }
+  }
+  if (tier[1] > tier[0] + g->n_split) {  // heavy
     auto k = k_big<ORIENT, MODE, BIG_CFG>;
     int grid = sms * occupancy(k, 256, sizeof(BigSM));
     // one overflow row + touched list per CTA, from the device's row pool
@@ -798,7 +992,7 @@ void launch_tiers(bf_graph* g, CountArgs a, const uint32_t tier[4], uint32_t* qu
     }
     a.orow = (uint32_t*)pool.p;                                  // [grid][orow_len]
     a.olist = (uint32_t*)pool.p + (size_t)grid * a.orow_len;     // [grid][olist_len]
-    a.t0 = tier[0]; a.t1 = tier[1]; a.queue = queues + 0;
+    a.t0 = tier[0] + g->n_split; a.t1 = tier[1]; a.queue = queues + 0;
     k<<<grid, 256, sizeof(BigSM), s>>>(a);
     KERNEL_CHECK(g);
   }
@@ -893,7 +1087,7 @@ bf_status graph_count(bf_graph* g, int mode, uint64_t* out_a, uint64_t* out_b, u
   for (int r = first; r <= last; r++) {
     a.rank = r;
     a.world = G;
-    CUDA_TRY(cudaMemsetAsync(g->queue.p, 0, 16, s));
+    CUDA_TRY(cudaMemsetAsync(g->queue.p, 0, 64, s));
     uint32_t* q = g->queue.as<uint32_t>();
     if (g->orient == BF_ORIENT_LOW) {
       if (mode == MODE_TOTAL) launch_tiers<BF_ORIENT_LOW, MODE_TOTAL>(g, a, tier, q, s);

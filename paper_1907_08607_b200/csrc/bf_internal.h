@@ -4,6 +4,7 @@
 #include <stdint.h>
 #include <stddef.h>
 #include <string>
+#include <vector>
 #include "../../include/bf.h"
 
 #define BF_SMS_DEFAULT 148
@@ -15,6 +16,9 @@
 #define BF_WARP_MAX_SLOTS 32u
 #define BF_MEDIUM_MAX_WEDGES 2048u
 #define BF_MEDIUM_MAX_SLOTS 128u
+// split starts: at most this many (largest first); row memory per batch
+constexpr uint32_t kMaxSplit = 4096;
+constexpr size_t kSplitRowBudget = (size_t)4 << 30;
 
 // ---- error plumbing --------------------------------------------------------
 void bf_set_error(const char* fmt, ...);
@@ -121,6 +125,24 @@ struct bf_graph {
   uint32_t n_tier[3] = {0, 0, 0};
   uint32_t t1 = 512, t2 = 2048;
 
+  // split starts (a4): the first n_split heavy starts (w > split threshold)
+  // are cut into pieces counted by many CTAs into one shared global d-row per
+  // start, then finalized separately.  Batches bound the rows' memory.
+  uint32_t n_split = 0;
+  uint64_t split_threshold = 0;
+  struct SplitBatch {
+    uint32_t s0, s1;      // split starts [s0, s1)
+    uint32_t p0, p1;      // their pieces [p0, p1)
+    uint64_t keys;        // row keys of the batch (sum of key ranges)
+  };
+  std::vector<SplitBatch> split_batches;
+  DevBuf split;      // uint4 [n_split] {s, j0, j1, -}
+  DevBuf split_off;  // u64 [n_split] row offset (keys) inside the batch's rows
+  DevBuf split_cnt;  // u32 [n_split] touched-list counts
+  DevBuf pieces;     // uint4 [n_pieces] {split index, slot begin, slot end, -}
+  DevBuf srow;       // u32 dense d-rows of the largest batch (kept zero between calls)
+  DevBuf slist;      // u32 touched lists (same layout as srow)
+
   // a5-a7: counting outputs / scratch
   DevBuf bv;      // u64 [n] per-vertex (rid space)
   DevBuf acc;     // u64 [2m] per-slot accumulators (edge mode)
@@ -140,7 +162,7 @@ struct bf_graph {
 
   template <class F> void for_each_buf(F f) {
     DevBuf* bufs[] = {&edges, &deg, &rid_of_gid, &gid_of_rid, &rkey, &off, &nbr, &pos, &hi, &where,
-                      &wstart, &seglo, &seglen, &wpre, &items, &order, &bv, &acc, &be, &total, &orow, &otouch, &queue, &hub,
+                      &wstart, &seglo, &seglen, &wpre, &items, &order, &bv, &acc, &be, &total, &orow, &otouch, &queue, &hub, &split, &split_off, &split_cnt, &pieces, &srow, &slist,
                       &tmp_a, &tmp_b, &tmp_c, &tmp_d, &tmp_e, &tmp_f, &tmp_scan};
     for (DevBuf* b : bufs) f(*b);
   }

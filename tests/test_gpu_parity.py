@@ -93,7 +93,7 @@ def test_random_small(bf, seed):
 
 @pytest.mark.parametrize("flags", ["warp", "cta", "dense", "small_window", "dense+small_window", "light8",
                                    "small_chunk", "dense+small_chunk", "dense+small_window+small_chunk",
-                                   "cta+small_window"])
+                                   "cta+small_window", "small_chunk+small_window", "dense+no_split+small_chunk"])
 @pytest.mark.parametrize("orient", ORIENTS)
 def test_forced_paths(bf, flags, orient):
     """T3: every start through one tier; tiny windows force the overflow paths
@@ -110,7 +110,9 @@ def test_forced_paths(bf, flags, orient):
     if "small_window" in flags:
         f |= bf.BF_FLAG_SMALL_WINDOW
     if "small_chunk" in flags:
-        f |= bf.BF_FLAG_SMALL_CHUNK
+        f |= bf.BF_FLAG_SMALL_CHUNK  # also drops the split threshold: giant-start pieces
+    if "no_split" in flags:
+        f |= bf.BF_FLAG_NO_SPLIT
     opts = dict(test_flags=f)
     if flags == "light8":
         opts["test_light_max_wedges"] = 8
