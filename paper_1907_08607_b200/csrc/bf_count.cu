@@ -175,7 +175,7 @@ __device__ __forceinline__ uint64_t* endpoint_slot(const CountArgs& a, uint32_t 
 
 // ------------------------------------------------ small counter store
 // u8 dense window over key offsets [0, wl) + open-addressed hash (u32 keys,
-// u32 counts) for the rest.  In the small tiers d(s,x) <= #slots of s <= 128
+// u8 counts) for the rest.  In the small tiers d(s,x) <= #slots of s <= 128
 // (each centre y in N(s) contributes at most one wedge per key), so u8 never
 // wraps.
 __device__ __forceinline__ uint32_t hslot(uint32_t key, uint32_t shift) { return (key * 0x9E3779B1u) >> shift; }
@@ -183,7 +183,7 @@ __device__ __forceinline__ uint32_t hslot(uint32_t key, uint32_t shift) { return
 struct SmallStore {
   uint32_t* win;  // u8 counters, four per word
   uint32_t* hk;
-  uint32_t* hv;
+  uint32_t* hv;   // u8 counts, four per word
   uint32_t wl, hmask, shift;
 
   // returns true if this increment took the key's count from 0 to 1
@@ -199,7 +199,10 @@ struct SmallStore {
     for (uint32_t probes = 0;; probes++) {
       if (probes > hmask) __trap();  // more distinct keys than slots: impossible by the tier bound
       const uint32_t cur = atomicCAS(hk + h, EMPTY, key);
-      if (cur == EMPTY || cur == key) return atomicAdd(hv + h, 1u) == 0u;
+      if (cur == EMPTY || cur == key) {
+        const uint32_t sh = (h & 3u) << 3;
+        return ((atomicAdd(hv + (h >> 2), 1u << sh) >> sh) & 0xffu) == 0u;
+      }
       h = (h + 1) & hmask;
     }
   }
@@ -210,7 +213,7 @@ struct SmallStore {
       if (probes > hmask) __trap();  // the key was inserted in pass 1
       h = (h + 1) & hmask;
     }
-    return hv[h];
+    return ((const uint8_t*)hv)[h];
   }
   __device__ __forceinline__ void zero(uint32_t kk) const {  // window keys only; the hash is cleared whole
     if (kk < wl) ((uint8_t*)win)[kk] = 0;
@@ -549,7 +552,7 @@ struct SmallSmem {
   Units<NT, UCAP> u;
   uint32_t win[WIN / 4];
   uint32_t hk[HS];
-  uint32_t hv[HS];
+  uint32_t hv[HS / 4];
   uint32_t list[CAP];   // distinct keys <= w <= CAP
   uint32_t cache[CAP];  // the start's keys in wedge order (pass 2 reads them here)
 };
@@ -584,7 +587,7 @@ __global__ void __launch_bounds__(NT, 1) k_small(CountArgs a) {
   cs.hmask = HS - 1;
   cs.shift = __clz(HS) + 1;  // 32 - log2(HS)
   for (uint32_t i = tid; i < WIN / 4; i += NT) ss.win[i] = 0;
-  for (uint32_t i = tid; i < HS; i += NT) { ss.hk[i] = EMPTY; ss.hv[i] = 0; }
+  for (uint32_t i = tid; i < HS; i += NT) { ss.hk[i] = EMPTY; if (i < HS / 4) ss.hv[i] = 0; }
   if (tid == 0) ss.u.lcnt = 0;
   cta_sync<NT>();
   uint64_t tot_acc = 0, pair_acc = 0;
@@ -627,7 +630,7 @@ __global__ void __launch_bounds__(NT, 1) k_small(CountArgs a) {
     if (NT == 32) hz = __any_sync(FULL, hashed);
     else hz = __syncthreads_or(hashed);
     if (hz) {
-      for (uint32_t i = tid; i < HS; i += NT) { ss.hk[i] = EMPTY; ss.hv[i] = 0; }
+      for (uint32_t i = tid; i < HS; i += NT) { ss.hk[i] = EMPTY; if (i < HS / 4) ss.hv[i] = 0; }
       cta_sync<NT>();
     }
     pf.mark(7);
@@ -867,10 +870,10 @@ __global__ void __launch_bounds__(256) k_split_clear(CountArgs a, SplitArgs sa) 
 
 // tier configurations <NT, WIN, HS|CAP, CAP|LCAP, P, G, UR>
 // warp tier: 1-warp CTAs, w <= 512, <= 32 slots
-#define WARP_CFG 32, 8192, 512, BF_WARP_MAX_WEDGES, 8, 4, 2
+#define WARP_CFG 32, 4096, 512, BF_WARP_MAX_WEDGES, 8, 4, 2
 using WarpSM = SmallSmem<WARP_CFG>;
 // medium tier: 128 threads, w <= 2048, <= 128 slots
-#define MED_CFG 128, 16384, 2048, BF_MEDIUM_MAX_WEDGES, 16, 4, 2
+#define MED_CFG 128, 8192, 2048, BF_MEDIUM_MAX_WEDGES, 16, 4, 2
 using MedSM = SmallSmem<MED_CFG>;
 // heavy tier: 256 threads, chunks of <= 8192 wedges
 #define BIG_CFG 256, 8192, 8192, 4096, 32, 4, 1
@@ -928,8 +931,10 @@ int occupancy(K kernel, int threads, size_t smem) {
 // held by graph_count for the whole call; a failed call marks the rows dirty.
 struct RowPool {
   std::mutex m;
-  void* p = nullptr;
+  void* p = nullptr;  // overflow rows, all zero between calls
   size_t bytes = 0;
+  void* l = nullptr;  // touched lists (scratch)
+  size_t lbytes = 0;
   bool dirty = false;
 };
 constexpr size_t kRowPoolBudget = (size_t)16 << 30;
@@ -980,18 +985,27 @@ void launch_tiers(bf_graph* g, CountArgs a, const uint32_t tier[4], uint32_t* qu
     const size_t row_bytes = (a.orow_len + a.olist_len) * 4;
     grid = (int)std::max<size_t>(1, std::min<size_t>((size_t)grid, kRowPoolBudget / row_bytes));
     RowPool& pool = row_pool(g->device);
-    const size_t need = (size_t)grid * row_bytes;
-    if (pool.bytes < need || pool.dirty) {
+    // rows (kept zero) and lists (scratch) are separate allocations, so a later
+    // launch with another grid never finds list garbage inside its rows
+    const size_t need_rows = (size_t)grid * a.orow_len * 4, need_lists = (size_t)grid * a.olist_len * 4;
+    if (pool.bytes < need_rows || pool.dirty) {
       if (pool.p) CUDA_TRY(cudaFree(pool.p));
       pool.p = nullptr;
       pool.bytes = 0;
-      CUDA_TRY(cudaMalloc(&pool.p, need));
-      pool.bytes = need;
-      CUDA_TRY(cudaMemsetAsync(pool.p, 0, need, s));
+      CUDA_TRY(cudaMalloc(&pool.p, need_rows));
+      pool.bytes = need_rows;
+      CUDA_TRY(cudaMemsetAsync(pool.p, 0, need_rows, s));
       pool.dirty = false;
     }
-    a.orow = (uint32_t*)pool.p;                                  // [grid][orow_len]
-    a.olist = (uint32_t*)pool.p + (size_t)grid * a.orow_len;     // [grid][olist_len]
+    if (pool.lbytes < need_lists) {
+      if (pool.l) CUDA_TRY(cudaFree(pool.l));
+      pool.l = nullptr;
+      pool.lbytes = 0;
+      CUDA_TRY(cudaMalloc(&pool.l, need_lists));
+      pool.lbytes = need_lists;
+    }
+    a.orow = (uint32_t*)pool.p;   // [grid][orow_len]
+    a.olist = (uint32_t*)pool.l;  // [grid][olist_len]
     a.t0 = tier[0] + g->n_split; a.t1 = tier[1]; a.queue = queues + 0;
     k<<<grid, 256, sizeof(BigSM), s>>>(a);
     KERNEL_CHECK(g);

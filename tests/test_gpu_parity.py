@@ -213,3 +213,19 @@ def test_csr_export(bf):
                     assert nbr[off[y] + pos[off[x] + i]] == x
             # per-start wedges (LOW orientation = Alg. 2 per x1)
             assert (c["wstart"][rid] == w_ref).all()
+
+
+@pytest.mark.parametrize("orient", ORIENTS)
+def test_repeated_graphs_same_process(bf, orient):
+    """Library state that outlives a graph (the per-device pool of heavy-tier
+    overflow rows) must be clean for the next graph, whatever the mode order."""
+    g = bfgen.config_graph(3, 0.01)
+    ref = oracle.count(g.n_u, g.n_v, g.edges, edge=False)
+    rank = bfgen.CONFIGS[3]["ranking"][0]
+    for rep in range(3):
+        for flags in (0, bf.BF_FLAG_FORCE_DENSE):
+            with bf.ButterflyGraph(g.n_u, g.n_v, g.edges, rank=rank, orient=orient, test_flags=flags) as bg:
+                assert bg.total() == ref["total"], (rep, flags)
+                bu, bv_, t = bg.vertex()
+                assert t == ref["total"] and np.array_equal(bu, ref["b_u"]) and np.array_equal(bv_, ref["b_v"])
+                assert bg.total() == ref["total"], (rep, flags)
