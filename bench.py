@@ -406,7 +406,7 @@ def main():
                        "note": "wedge kernel alone (CUDA events around its launch on the graph's stream)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                     "kernel": f"k_count<{orient_name},{a.mode}>",
+                     "kernel": "wedge kernels (k_split_walk/k_split_finalize, k_big, k_small x2) of one bf_count call",
                      "algorithmic_bytes": abytes, "P_pairs": P,
                      "bytes_model": {"vertex": "8W+48m+16P+28n", "edge": "28W+52m+12n",
                                      "total": "4W+16m+12n"}[a.mode],
