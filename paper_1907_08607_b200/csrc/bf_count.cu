@@ -76,9 +76,7 @@ struct CountArgs {
   uint64_t S, n;          // slots, vertices (bounds checks of the debug build)
   uint32_t dbg_stop;      // debug build: stop each start after this phase (0 = never)
   uint32_t exp;           // timing experiments (env BF_EXPERIMENT; results are wrong when set):
-                          // 1 = skip endpoint REDs, 2 = skip centre REDs, 4 = pass 1 loads
-                          // keys but skips the counters, 8 = pass 1 fakes keys without loads,
-                          // 16 = no owner lists
+                          // 1 = skip endpoint REDs, 2 = skip centre REDs
   uint32_t win;           // dense window keys in use (<= compile-time size)
   uint32_t cap;           // heavy chunk capacity in wedges (<= HV_CAP)
   int rank, world;
@@ -215,8 +213,17 @@ struct SmallStore {
     }
     return ((const uint8_t*)hv)[h];
   }
-  __device__ __forceinline__ void zero(uint32_t kk) const {  // window keys only; the hash is cleared whole
-    if (kk < wl) ((uint8_t*)win)[kk] = 0;
+  // reset one key (every key of the start is reset, so deleting hash entries
+  // never strands a lookup: get() probes past EMPTY slots)
+  __device__ __forceinline__ void zero(uint32_t key, uint32_t kk) const {
+    if (kk < wl) {
+      ((uint8_t*)win)[kk] = 0;
+      return;
+    }
+    uint32_t h = hslot(key, shift);
+    while (hk[h] != key) h = (h + 1) & hmask;
+    hk[h] = EMPTY;
+    ((uint8_t*)hv)[h] = 0;
   }
 };
 
@@ -236,7 +243,7 @@ struct HeavyStore {
   __device__ __forceinline__ uint32_t get(uint32_t, uint32_t kk) const {
     return kk < wl ? win[kk] : __ldcg(orow + (kk - wl));
   }
-  __device__ __forceinline__ void zero(uint32_t kk) const {
+  __device__ __forceinline__ void zero(uint32_t, uint32_t kk) const {
     if (kk < wl) win[kk] = 0;
     else __stcg(orow + (kk - wl), 0u);
   }
@@ -292,10 +299,10 @@ __device__ __forceinline__ void units_write(Units<NT, UCAP>& u, uint32_t lo, uin
   const uint32_t pk = cta_scan<NT>((L << 16) | nu, u.wt, total);
   const uint32_t ex = pk & 0xffffu, wp = pk >> 16;
   BF_CHECK(ex + nu <= UCAP && L < 65536);
-  for (uint32_t f = 0; f < nu; f++) {
-    u.lo[ex + f] = lo + (f << LP);
-    u.pos[ex + f] = (uint16_t)(wp + (f << LP));
-    u.len[ex + f] = (uint8_t)min(L - (f << LP), (uint32_t)P);
+  for (uint32_t f = 0, o = 0; f < nu; f++, o += P) {
+    u.lo[ex + f] = lo + o;
+    u.pos[ex + f] = (uint16_t)(wp + o);
+    u.len[ex + f] = (uint8_t)(f + 1 < nu ? (uint32_t)P : L - o);
     u.slot[ex + f] = (typename Units<NT, UCAP>::SlotT)threadIdx.x;
   }
   if (threadIdx.x == 0) u.nunits = total & 0xffffu;
@@ -340,21 +347,25 @@ __device__ __forceinline__ uint64_t units_build(const CountArgs& a, Units<NT, UC
 
 // owner of a key (its count went 0 -> 1): append it to the start's list
 // (shared memory up to lcap entries, then the CTA's global list)
+// SPILL: the list can outgrow shared memory (heavy tier); otherwise lcap is
+// an exact bound (small tiers: distinct keys <= w <= lcap)
+template <bool SPILL>
 __device__ __forceinline__ void list_push(uint32_t* lcnt, uint32_t* list, uint32_t lcap, uint32_t* olist,
                                           uint64_t ocap, uint32_t key) {
   const uint32_t i = atomicAdd(lcnt, 1u);
-  if (i < lcap) list[i] = key;
+  if (!SPILL || i < lcap) list[i] = key;
   else {
     BF_CHECK(olist != nullptr && i - lcap < ocap);
     olist[i - lcap] = key;
   }
 }
+template <bool SPILL>
 __device__ __forceinline__ uint32_t list_get(const uint32_t* list, uint32_t lcap, const uint32_t* olist, uint32_t i) {
-  return i < lcap ? list[i] : __ldcg(olist + (i - lcap));
+  return (!SPILL || i < lcap) ? list[i] : __ldcg(olist + (i - lcap));
 }
 
 // pass 1 over the chunk's units: d(key) += 1 per wedge
-template <int NT, int P, int G, int UR, uint32_t UCAP, class Store>
+template <bool SPILL, bool CACHE, int NT, int P, int G, int UR, uint32_t UCAP, class Store>
 __device__ __forceinline__ void units_pass1(const CountArgs& a, Units<NT, UCAP>& u, const Store& cs,
                                             uint32_t kbase, uint32_t* list, uint32_t lcap, uint32_t* olist,
                                             bool& hashed, uint32_t* cache) {
@@ -373,7 +384,7 @@ __device__ __forceinline__ void units_pass1(const CountArgs& a, Units<NT, UCAP>&
       for (int it = 0; it < IT; it++) {
         const uint32_t i = gl + it * G;
         BF_CHECK(i >= len || lo + i < a.S);
-        key[r][it] = i < len ? ((a.exp & 8) ? kbase + ((lo + i) & 4095u) : __ldg(a.nbr + (lo + i))) : EMPTY;
+        key[r][it] = i < len ? __ldg(a.nbr + (lo + i)) : EMPTY;
       }
     }
 #pragma unroll
@@ -383,9 +394,8 @@ __device__ __forceinline__ void units_pass1(const CountArgs& a, Units<NT, UCAP>&
         const uint32_t k = key[r][it];
         if (k != EMPTY) {
           BF_CHECK(k < a.n);
-          if (cache) cache[ps[r] + gl + it * G] = k;
-          if (a.exp & 4) { hashed |= (k == 0xFFFFFFFEu); continue; }  // experiment: loads only
-          if (cs.add(k, k - kbase, hashed) && !(a.exp & 16)) list_push(&u.lcnt, list, lcap, olist, a.olist_len, k);
+          if (CACHE) cache[ps[r] + gl + it * G] = k;
+          if (cs.add(k, k - kbase, hashed)) list_push<SPILL>(&u.lcnt, list, lcap, olist, a.olist_len, k);
         }
       }
   }
@@ -394,7 +404,7 @@ __device__ __forceinline__ void units_pass1(const CountArgs& a, Units<NT, UCAP>&
 // pass 2 over the chunk's units: c = d(key) - 1 per wedge, summed per slot
 // (centre y in vertex mode, edge (s, y) in edge mode); edge mode also adds c
 // to the wedge's (y, key) edge
-template <int MODE, int NT, int P, int G, int UR, uint32_t UCAP, class Store>
+template <int MODE, bool CACHE, int NT, int P, int G, int UR, uint32_t UCAP, class Store>
 __device__ __forceinline__ void units_pass2(const CountArgs& a, Units<NT, UCAP>& u, const Store& cs,
                                             uint32_t kbase, const uint32_t* cache) {
   constexpr int IT = P / G;
@@ -413,7 +423,7 @@ __device__ __forceinline__ void units_pass2(const CountArgs& a, Units<NT, UCAP>&
 #pragma unroll
       for (int it = 0; it < IT; it++) {
         const uint32_t i = gl + it * G;
-        key[r][it] = i < len ? (cache ? cache[ps + i] : __ldg(a.nbr + (lo[r] + i))) : EMPTY;
+        key[r][it] = i < len ? (CACHE ? cache[ps + i] : __ldg(a.nbr + (lo[r] + i))) : EMPTY;
       }
     }
 #pragma unroll
@@ -449,15 +459,15 @@ __device__ __forceinline__ void slot_flush(const CountArgs& a, const uint32_t* s
 
 // finalize over the owner list: C(d,2) to the total and both endpoints (total
 // mode also resets the counters here)
-template <int MODE, int NT, class Store>
+template <int MODE, bool SPILL, int NT, class Store>
 __device__ __forceinline__ void list_finalize(const CountArgs& a, const Store& cs, uint32_t kbase, uint32_t cnt,
                                               const uint32_t* list, uint32_t lcap, const uint32_t* olist,
                                               uint64_t& lsum) {
   for (uint32_t i = threadIdx.x; i < cnt; i += NT) {
-    const uint32_t key = list_get(list, lcap, olist, i), kk = key - kbase;
+    const uint32_t key = list_get<SPILL>(list, lcap, olist, i), kk = key - kbase;
     BF_CHECK(key < a.n);
     const uint32_t d = cs.get(key, kk);
-    if (MODE == MODE_TOTAL) cs.zero(kk);
+    if (MODE == MODE_TOTAL) cs.zero(key, kk);
     const uint64_t c2 = choose2(d);
     lsum += c2;
     if (MODE == MODE_VERTEX && c2 && !(a.exp & 1)) red_add_u64(endpoint_slot(a, key), c2);
@@ -476,7 +486,7 @@ __device__ __forceinline__ void list_finalize(const CountArgs& a, const Store& c
 // The rest of a start once its (first) chunk's units are built: pass 1,
 // finalize, pass 2, reset.  `single`: the whole start is that one chunk
 // (units reused by pass 2); otherwise chunks are rebuilt by units_build.
-template <int ORIENT, int MODE, int NT, int P, int G, int UR, uint32_t UCAP, class Store>
+template <int ORIENT, int MODE, bool SPILL, bool CACHE, int NT, int P, int G, int UR, uint32_t UCAP, class Store>
 __device__ __forceinline__ void start_passes(const CountArgs& a, Units<NT, UCAP>& u, const Store& cs,
                                              const Start& st, bool single, uint64_t base, uint64_t w, uint64_t K1,
                                              uint32_t cap, uint32_t jn0, bool mine, uint32_t myj, uint32_t myy,
@@ -484,7 +494,8 @@ __device__ __forceinline__ void start_passes(const CountArgs& a, Units<NT, UCAP>
                                              uint64_t& pairs, bool& hashed, Prof& pf, uint32_t* cache) {
   const uint32_t tid = threadIdx.x;
   // ---- pass 1 (first chunk already built)
-  units_pass1<NT, P, G, UR, UCAP>(a, u, cs, st.kbase, list, lcap, olist, hashed, single ? cache : nullptr);
+  if (single) units_pass1<SPILL, CACHE, NT, P, G, UR, UCAP>(a, u, cs, st.kbase, list, lcap, olist, hashed, cache);
+  else units_pass1<SPILL, false, NT, P, G, UR, UCAP>(a, u, cs, st.kbase, list, lcap, olist, hashed, nullptr);
   pf.mark(2);
   cta_sync<NT>();
   pf.mark(3);
@@ -495,7 +506,7 @@ __device__ __forceinline__ void start_passes(const CountArgs& a, Units<NT, UCAP>
     while (K0 < w) {
       const uint64_t Kn = units_build<MODE, NT, P, UCAP>(a, u, jc, st.j1, base, K0, cap, par, mine, myj, myy);
       const uint32_t jn = u.jn[par];
-      units_pass1<NT, P, G, UR, UCAP>(a, u, cs, st.kbase, list, lcap, olist, hashed, nullptr);
+      units_pass1<SPILL, false, NT, P, G, UR, UCAP>(a, u, cs, st.kbase, list, lcap, olist, hashed, nullptr);
       cta_sync<NT>();
       if (tid == 0) u.jn[par] = FULL;
       jc = jn != FULL ? jn : ((st.j1 - jc > (uint32_t)NT) ? jc + NT : st.j1);
@@ -505,14 +516,14 @@ __device__ __forceinline__ void start_passes(const CountArgs& a, Units<NT, UCAP>
   }
   pf.mark(1);
   const uint32_t cnt = u.lcnt;
-  list_finalize<MODE, NT>(a, cs, st.kbase, cnt, list, lcap, olist, lsum);
+  list_finalize<MODE, SPILL, NT>(a, cs, st.kbase, cnt, list, lcap, olist, lsum);
   if (tid == 0) pairs += cnt;
   pf.mark(4);
   if (MODE != MODE_TOTAL) {
     cta_sync<NT>();  // d is final
     pf.mark(3);
     if (single) {
-      units_pass2<MODE, NT, P, G, UR, UCAP>(a, u, cs, st.kbase, cache);
+      units_pass2<MODE, CACHE, NT, P, G, UR, UCAP>(a, u, cs, st.kbase, cache);
       pf.mark(5);
       cta_sync<NT>();
       pf.mark(3);
@@ -523,7 +534,7 @@ __device__ __forceinline__ void start_passes(const CountArgs& a, Units<NT, UCAP>
       while (K0 < w) {
         const uint64_t Kn = units_build<MODE, NT, P, UCAP>(a, u, jc, st.j1, base, K0, cap, par, mine, myj, myy);
         const uint32_t jn = u.jn[par];
-        units_pass2<MODE, NT, P, G, UR, UCAP>(a, u, cs, st.kbase, nullptr);
+        units_pass2<MODE, false, NT, P, G, UR, UCAP>(a, u, cs, st.kbase, nullptr);
         cta_sync<NT>();
         if (tid == 0) u.jn[par] = FULL;
         slot_flush<MODE>(a, u.slo, u.shi, mine, myj, myy);
@@ -532,7 +543,10 @@ __device__ __forceinline__ void start_passes(const CountArgs& a, Units<NT, UCAP>
         par ^= 1u;
       }
     }
-    for (uint32_t i = tid; i < cnt; i += NT) cs.zero(list_get(list, lcap, olist, i) - st.kbase);
+    for (uint32_t i = tid; i < cnt; i += NT) {
+      const uint32_t key = list_get<SPILL>(list, lcap, olist, i);
+      cs.zero(key, key - st.kbase);
+    }
   }
   pf.mark(6);
   cta_sync<NT>();
@@ -618,20 +632,13 @@ __global__ void __launch_bounds__(NT, 1) k_small(CountArgs a) {
     pf.mark(1);
     uint64_t lsum = 0;
     bool hashed = false;
-    start_passes<ORIENT, MODE, NT, P, G, UR, SM::UCAP>(a, ss.u, cs, st, true, 0, 0, 0, CAP, FULL, sr.len != 0,
+    start_passes<ORIENT, MODE, false, true, NT, P, G, UR, SM::UCAP>(a, ss.u, cs, st, true, 0, 0, 0, CAP, FULL, sr.len != 0,
                                                        st.j0 + tid, sr.y, ss.list, CAP, nullptr, lsum, pair_acc,
                                                        hashed, pf, ss.cache);
     tot_acc += lsum;
     if (MODE == MODE_VERTEX) {
       const uint64_t t = warp_sum(lsum);
       if (lane == 0 && t) red_add_u64(a.bv + st.s, t);
-    }
-    bool hz;
-    if (NT == 32) hz = __any_sync(FULL, hashed);
-    else hz = __syncthreads_or(hashed);
-    if (hz) {
-      for (uint32_t i = tid; i < HS; i += NT) { ss.hk[i] = EMPTY; if (i < HS / 4) ss.hv[i] = 0; }
-      cta_sync<NT>();
     }
     pf.mark(7);
     if (itn == EMPTY) break;
@@ -689,7 +696,7 @@ __global__ void __launch_bounds__(NT, 1) k_big(CountArgs a) {
     const uint32_t jn0 = hs.u.jn[0];
     uint64_t lsum = 0;
     bool hashed = false;
-    start_passes<ORIENT, MODE, NT, P, G, UR, SM::UCAP>(a, hs.u, cs, st, single, base, w, K1, cap, jn0, mine, myj,
+    start_passes<ORIENT, MODE, true, false, NT, P, G, UR, SM::UCAP>(a, hs.u, cs, st, single, base, w, K1, cap, jn0, mine, myj,
                                                        myy, hs.list, LCAP, olist, lsum, pair_acc, hashed, pf,
                                                        (uint32_t*)nullptr);
     tot_acc += lsum;
@@ -791,8 +798,8 @@ __global__ void __launch_bounds__(SP_NT, 1) k_split_walk(CountArgs a, SplitArgs 
       const uint64_t K1 = units_build<PASS2 ? MODE : MODE_TOTAL, SP_NT, SP_P, SplitSmem::UCAP>(
           a, ss.u, jc, pc.z, base, K0, cap, par, mine, myj, myy);
       const uint32_t jn = ss.u.jn[par];
-      if (PASS2) units_pass2<MODE, SP_NT, SP_P, SP_G, 1, SplitSmem::UCAP>(a, ss.u, s2, kbase, nullptr);
-      else units_pass1<SP_NT, SP_P, SP_G, 1, SplitSmem::UCAP>(a, ss.u, s1, kbase, ss.list, SP_WIN, nullptr, hashed,
+      if (PASS2) units_pass2<MODE, false, SP_NT, SP_P, SP_G, 1, SplitSmem::UCAP>(a, ss.u, s2, kbase, nullptr);
+      else units_pass1<false, false, SP_NT, SP_P, SP_G, 1, SplitSmem::UCAP>(a, ss.u, s1, kbase, ss.list, SP_WIN, nullptr, hashed,
                                                               nullptr);
       __syncthreads();
       if (tid == 0) ss.u.jn[par] = FULL;
