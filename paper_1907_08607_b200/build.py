@@ -30,15 +30,19 @@ def needs_build() -> bool:
     return any(os.path.getmtime(p) > t for p in deps())
 
 
-def build(force: bool = False, verbose: bool = False, debug: bool = False, profile: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, debug: bool = False, profile: bool = False,
+          variant: str = "", defines: tuple = ()) -> str:
     """debug=True builds libbf_debug.so (device bounds checks, -DBF_DEBUG);
     profile=True builds libbf_prof.so (per-phase clock64 timing, -DBF_PROFILE).
     Load either with BF_LIB=<name>."""
     so = SO.replace("libbf.so", "libbf_debug.so") if debug else (SO.replace("libbf.so", "libbf_prof.so") if profile else SO)
-    if not force and not debug and not profile and not needs_build():
+    if variant:  # tuning experiments: libbf_<variant>.so with extra -D defines
+        so = SO.replace("libbf.so", f"libbf_{variant}.so")
+    if not force and not debug and not profile and not variant and not needs_build():
         return SO
     cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "--shared", "-Xcompiler", "-fPIC", "-Xptxas", "-v" if verbose else "-O3",
            *(["-DBF_DEBUG"] if debug else []), *(["-DBF_PROFILE"] if profile else []),
+           *[f"-D{d}" for d in defines],
            "-I", os.path.join(HERE, "..", "include"), "-o", so + ".tmp", *sources(), "-ldl"]
     subprocess.check_call(cmd)
     os.replace(so + ".tmp", so)

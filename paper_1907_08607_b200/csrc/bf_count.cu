@@ -179,7 +179,8 @@ __device__ __forceinline__ uint64_t* endpoint_slot(const CountArgs& a, uint32_t 
 __device__ __forceinline__ uint32_t hslot(uint32_t key, uint32_t shift) { return (key * 0x9E3779B1u) >> shift; }
 
 struct SmallStore {
-  uint32_t* win;  // u8 counters, four per word
+  uint32_t* win;  // u8 counters, four per word (key kk: word kk & w4m, byte kk >> w4s)
+  uint32_t w4m, w4s;
   uint32_t* hk;
   uint32_t* hv;   // u8 counts, four per word
   uint32_t wl, hmask, shift;
@@ -187,9 +188,11 @@ struct SmallStore {
   // returns true if this increment took the key's count from 0 to 1
   __device__ __forceinline__ bool add(uint32_t key, uint32_t kk, bool& hashed) const {
     if (kk < wl) {
-      BF_CHECK(__isShared(win + (kk >> 2)));
-      const uint32_t sh = (kk & 3u) << 3;
-      const uint32_t old = atomicAdd(win + (kk >> 2), 1u << sh);
+      // key kk lives in byte kk >> w4s of word kk & w4m: neighbouring keys (the
+      // hottest hubs are rids 0, 1, 2, ...) never share a word or a bank
+      BF_CHECK(__isShared(win + (kk & w4m)));
+      const uint32_t sh = (kk >> w4s) << 3;
+      const uint32_t old = atomicAdd(win + (kk & w4m), 1u << sh);
       return ((old >> sh) & 0xffu) == 0u;
     }
     hashed = true;
@@ -205,7 +208,7 @@ struct SmallStore {
     }
   }
   __device__ __forceinline__ uint32_t get(uint32_t key, uint32_t kk) const {
-    if (kk < wl) return ((const uint8_t*)win)[kk];
+    if (kk < wl) return ((const uint8_t*)win)[((kk & w4m) << 2) | (kk >> w4s)];
     uint32_t h = hslot(key, shift);
     for (uint32_t probes = 0; hk[h] != key; probes++) {
       if (probes > hmask) __trap();  // the key was inserted in pass 1
@@ -217,7 +220,7 @@ struct SmallStore {
   // never strands a lookup: get() probes past EMPTY slots)
   __device__ __forceinline__ void zero(uint32_t key, uint32_t kk) const {
     if (kk < wl) {
-      ((uint8_t*)win)[kk] = 0;
+      ((uint8_t*)win)[((kk & w4m) << 2) | (kk >> w4s)] = 0;
       return;
     }
     uint32_t h = hslot(key, shift);
@@ -391,7 +394,8 @@ __device__ __forceinline__ void units_pass1(const CountArgs& a, Units<NT, UCAP>&
     for (int r = 0; r < UR; r++)
 #pragma unroll
       for (int it = 0; it < IT; it++) {
-        const uint32_t k = key[r][it];
+        uint32_t k = key[r][it];
+        if ((a.exp & 32) && k != EMPTY) k = kbase + (((k - kbase) * 0x9E3779B1u) >> 20);  // timing only: scatter hub keys
         if (k != EMPTY) {
           BF_CHECK(k < a.n);
           if (CACHE) cache[ps[r] + gl + it * G] = k;
@@ -592,9 +596,11 @@ __global__ void __launch_bounds__(NT, 1) k_small(CountArgs a) {
   extern __shared__ __align__(16) char sm[];
   SM& ss = *(SM*)sm;
   const uint32_t tid = threadIdx.x, lane = tid & 31;
-  static_assert((HS & (HS - 1)) == 0 && WIN % 4 == 0, "store sizes");
+  static_assert((HS & (HS - 1)) == 0 && (WIN & (WIN - 1)) == 0 && WIN >= 4, "store sizes");
   SmallStore cs;
   cs.win = ss.win;
+  cs.w4m = WIN / 4 - 1;
+  cs.w4s = 31 - __clz(WIN / 4);
   cs.hk = ss.hk;
   cs.hv = ss.hv;
   cs.wl = min(a.win, WIN);
@@ -877,14 +883,35 @@ __global__ void __launch_bounds__(256) k_split_clear(CountArgs a, SplitArgs sa) 
 
 // tier configurations <NT, WIN, HS|CAP, CAP|LCAP, P, G, UR>
 // warp tier: 1-warp CTAs, w <= 512, <= 32 slots
-#define WARP_CFG 32, 4096, 512, BF_WARP_MAX_WEDGES, 8, 4, 2
+#ifndef BF_WARP_WIN
+#define BF_WARP_WIN 4096
+#endif
+#ifndef BF_MED_WIN
+#define BF_MED_WIN 8192
+#endif
+#ifndef BF_BIG_WIN
+#define BF_BIG_WIN 8192
+#endif
+#define WARP_CFG 32, BF_WARP_WIN, 512, BF_WARP_MAX_WEDGES, 8, 4, 2
 using WarpSM = SmallSmem<WARP_CFG>;
 // medium tier: 128 threads, w <= 2048, <= 128 slots
-#define MED_CFG 128, 8192, 2048, BF_MEDIUM_MAX_WEDGES, 16, 4, 2
+#define MED_CFG 128, BF_MED_WIN, 2048, BF_MEDIUM_MAX_WEDGES, 16, 4, 2
 using MedSM = SmallSmem<MED_CFG>;
 // heavy tier: 256 threads, chunks of <= 8192 wedges
-#define BIG_CFG 256, 8192, 8192, 4096, 32, 4, 1
-constexpr uint64_t HV_WIN_KEYS = 8192;  // BIG_CFG's window
+#ifndef BF_BIG_NT
+#define BF_BIG_NT 256
+#endif
+#ifndef BF_BIG_CAP
+#define BF_BIG_CAP 8192
+#endif
+#ifndef BF_BIG_LCAP
+#define BF_BIG_LCAP 4096
+#endif
+#ifndef BF_BIG_P
+#define BF_BIG_P 32
+#endif
+#define BIG_CFG BF_BIG_NT, BF_BIG_WIN, BF_BIG_CAP, BF_BIG_LCAP, BF_BIG_P, 4, 1
+constexpr uint64_t HV_WIN_KEYS = BF_BIG_WIN;  // BIG_CFG's window
 using BigSM = HeavySmemT<BIG_CFG>;
 static_assert(BF_WARP_MAX_SLOTS == 32 && BF_MEDIUM_MAX_SLOTS == 128, "tier slot bounds = CTA sizes");
 
@@ -984,7 +1011,7 @@ void launch_tiers(bf_graph* g, CountArgs a, const uint32_t tier[4], uint32_t* qu
   }
   if (tier[1] > tier[0] + g->n_split) {  // heavy
     auto k = k_big<ORIENT, MODE, BIG_CFG>;
-    int grid = sms * occupancy(k, 256, sizeof(BigSM));
+    int grid = sms * occupancy(k, BF_BIG_NT, sizeof(BigSM));
     // one overflow row + touched list per CTA, from the device's row pool
     // (rows are kept zero by the owners' resets, so a clean pool is reused
     // across graphs without clearing); the grid shrinks if the rows of every
@@ -1014,7 +1041,7 @@ void launch_tiers(bf_graph* g, CountArgs a, const uint32_t tier[4], uint32_t* qu
     a.orow = (uint32_t*)pool.p;   // [grid][orow_len]
     a.olist = (uint32_t*)pool.l;  // [grid][olist_len]
     a.t0 = tier[0] + g->n_split; a.t1 = tier[1]; a.queue = queues + 0;
-    k<<<grid, 256, sizeof(BigSM), s>>>(a);
+    k<<<grid, BF_BIG_NT, sizeof(BigSM), s>>>(a);
     KERNEL_CHECK(g);
   }
   if (tier[2] > tier[1]) {  // medium
