@@ -558,6 +558,55 @@ __device__ __forceinline__ void start_passes(const CountArgs& a, Units<NT, UCAP>
   if (tid == 0) u.lcnt = 0;
 }
 
+// ------------------------------------------------------------- slot mode
+// Starts whose segments are short on average (c4's item starts: a few wedges
+// per slot) waste most lanes of a P-wedge unit and most of a chunk's barriers.
+// They run in slot mode instead: thread per slot, walking its segment with
+// four predicated loads in flight; pass-2 sums stay in a register per slot.
+constexpr uint32_t SLOT_MODE_AVG = 6;  // slot mode when w < 6 * #slots
+
+template <bool SPILL, int NT, class Store>
+__device__ __forceinline__ void slots_pass1(const CountArgs& a, const Store& cs, uint32_t j0, uint32_t j1,
+                                            uint32_t kbase, uint32_t* lcnt, uint32_t* list, uint32_t lcap,
+                                            uint32_t* olist, bool& hashed) {
+  for (uint32_t j = j0 + threadIdx.x; j < j1; j += NT) {
+    const uint32_t len = __ldg(a.seglen + j), lo = __ldg(a.seglo + j);
+    for (uint32_t i0 = 0; i0 < len; i0 += 4) {
+      uint32_t k[4];
+#pragma unroll
+      for (int t = 0; t < 4; t++) k[t] = i0 + t < len ? __ldg(a.nbr + (lo + i0 + t)) : EMPTY;
+#pragma unroll
+      for (int t = 0; t < 4; t++)
+        if (k[t] != EMPTY && cs.add(k[t], k[t] - kbase, hashed)) list_push<SPILL>(lcnt, list, lcap, olist, a.olist_len, k[t]);
+    }
+  }
+}
+
+template <int MODE, int NT, class Store>
+__device__ __forceinline__ void slots_pass2(const CountArgs& a, const Store& cs, uint32_t j0, uint32_t j1,
+                                            uint32_t kbase) {
+  for (uint32_t j = j0 + threadIdx.x; j < j1; j += NT) {
+    const uint32_t len = __ldg(a.seglen + j), lo = __ldg(a.seglo + j);
+    uint64_t s = 0;
+    for (uint32_t i0 = 0; i0 < len; i0 += 4) {
+      uint32_t k[4];
+#pragma unroll
+      for (int t = 0; t < 4; t++) k[t] = i0 + t < len ? __ldg(a.nbr + (lo + i0 + t)) : EMPTY;
+#pragma unroll
+      for (int t = 0; t < 4; t++)
+        if (k[t] != EMPTY) {
+          const uint32_t c = cs.get(k[t], k[t] - kbase) - 1u;
+          s += c;
+          if (MODE == MODE_EDGE && c) red_add_u64(a.acc + (lo + i0 + t), c);  // edge (y, key)
+        }
+    }
+    if (s) {
+      if (MODE == MODE_VERTEX) { if (!(a.exp & 2)) red_add_u64(a.bv + __ldg(a.nbr + j), s); }  // centre y
+      else red_add_u64(a.acc + j, s);                                                        // edge (s, y)
+    }
+  }
+}
+
 // ------------------------------------------------------------- small tiers
 // warp / medium: u8 dense window + shared hash; one chunk per start (w <= CAP,
 // slots <= NT).  Starts are taken in a static stride (the tier is sorted by
@@ -695,16 +744,35 @@ __global__ void __launch_bounds__(NT, 1) k_big(CountArgs a) {
     const uint64_t base = __ldg(a.wpre + st.j0);
     const uint64_t w = __ldg(a.wpre + st.j1) - base;
     const bool single = w <= cap && st.j1 - st.j0 <= (uint32_t)NT;
-    bool mine;
-    uint32_t myj, myy;
-    pf.mark(0);
-    const uint64_t K1 = units_build<MODE, NT, P, SM::UCAP>(a, hs.u, st.j0, st.j1, base, 0, cap, 0, mine, myj, myy);
-    const uint32_t jn0 = hs.u.jn[0];
     uint64_t lsum = 0;
     bool hashed = false;
-    start_passes<ORIENT, MODE, true, false, NT, P, G, UR, SM::UCAP>(a, hs.u, cs, st, single, base, w, K1, cap, jn0, mine, myj,
-                                                       myy, hs.list, LCAP, olist, lsum, pair_acc, hashed, pf,
-                                                       (uint32_t*)nullptr);
+    pf.mark(0);
+    if (w < (uint64_t)SLOT_MODE_AVG * (st.j1 - st.j0)) {  // short segments: slot mode
+      slots_pass1<true, NT>(a, cs, st.j0, st.j1, st.kbase, &hs.u.lcnt, hs.list, LCAP, olist, hashed);
+      __syncthreads();
+      const uint32_t cnt = hs.u.lcnt;
+      list_finalize<MODE, true, NT>(a, cs, st.kbase, cnt, hs.list, LCAP, olist, lsum);
+      if (tid == 0) pair_acc += cnt;
+      if (MODE != MODE_TOTAL) {
+        __syncthreads();
+        slots_pass2<MODE, NT>(a, cs, st.j0, st.j1, st.kbase);
+        __syncthreads();
+        for (uint32_t i = tid; i < cnt; i += NT) {
+          const uint32_t key = list_get<true>(hs.list, LCAP, olist, i);
+          cs.zero(key, key - st.kbase);
+        }
+      }
+      __syncthreads();
+      if (tid == 0) hs.u.lcnt = 0;
+    } else {
+      bool mine;
+      uint32_t myj, myy;
+      const uint64_t K1 = units_build<MODE, NT, P, SM::UCAP>(a, hs.u, st.j0, st.j1, base, 0, cap, 0, mine, myj, myy);
+      const uint32_t jn0 = hs.u.jn[0];
+      start_passes<ORIENT, MODE, true, false, NT, P, G, UR, SM::UCAP>(a, hs.u, cs, st, single, base, w, K1, cap, jn0,
+                                                                      mine, myj, myy, hs.list, LCAP, olist, lsum,
+                                                                      pair_acc, hashed, pf, (uint32_t*)nullptr);
+    }
     tot_acc += lsum;
     if (MODE == MODE_VERTEX) {
       const uint64_t t = warp_sum(lsum);
@@ -798,6 +866,12 @@ __global__ void __launch_bounds__(SP_NT, 1) k_split_walk(CountArgs a, SplitArgs 
     uint32_t jc = pc.y, par = 0;
     uint64_t K0 = 0;
     bool hashed = false;
+    if (w < (uint64_t)SLOT_MODE_AVG * (pc.z - pc.y)) {  // short segments: slot mode
+      if (PASS2) slots_pass2<MODE, SP_NT>(a, s2, pc.y, pc.z, kbase);
+      else slots_pass1<false, SP_NT>(a, s1, pc.y, pc.z, kbase, &ss.u.lcnt, ss.list, SP_WIN, nullptr, hashed);
+      __syncthreads();
+      K0 = w;  // skip the unit walk
+    }
     while (K0 < w) {
       bool mine;
       uint32_t myj, myy;
