@@ -25,13 +25,31 @@ inline unsigned grid_for(size_t n, int sms) {
 }
 
 // ---- a1 -----------------------------------------------------------------------
+// degree increments are aggregated over the lanes of a warp that hold the same
+// vertex (__match_any_sync): power-law hubs (c4's Zipf items) would otherwise
+// serialise thousands of atomics on one address
+__device__ __forceinline__ void add_degree(uint32_t* deg, uint64_t z, bool valid) {
+  const uint32_t act = __ballot_sync(0xffffffffu, valid);
+  if (!valid) return;
+  const uint32_t peers = __match_any_sync(act, (unsigned long long)z);
+  if ((threadIdx.x & 31) == (uint32_t)(__ffs(peers) - 1)) atomicAdd(&deg[z], (uint32_t)__popc(peers));
+}
+
 __global__ void k_validate_degree(const uint32_t* __restrict__ e, uint64_t m, uint32_t nU, uint32_t nV,
                                   uint32_t* __restrict__ deg, uint32_t* __restrict__ flags) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
-    uint2 uv = reinterpret_cast<const uint2*>(e)[i];
-    if (uv.x >= nU || uv.y >= nV) { atomicOr(flags, 1u); continue; }
-    atomicAdd(&deg[uv.x], 1u);
-    atomicAdd(&deg[(uint64_t)nU + uv.y], 1u);
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  // warp-uniform trip count (the aggregation is a warp collective)
+  for (uint64_t i0 = blockIdx.x * (uint64_t)blockDim.x + (threadIdx.x & ~31u); i0 < m; i0 += stride) {
+    const uint64_t i = i0 + (threadIdx.x & 31);
+    uint2 uv = make_uint2(0, 0);
+    bool ok = false;
+    if (i < m) {
+      uv = reinterpret_cast<const uint2*>(e)[i];
+      ok = uv.x < nU && uv.y < nV;
+      if (!ok) atomicOr(flags, 1u);
+    }
+    add_degree(deg, uv.x, ok);
+    add_degree(deg, (uint64_t)nU + uv.y, ok);
   }
 }
 
