@@ -12,9 +12,13 @@
 // work-plan tiers (a4): warp tier for w <= BF_WARP_MAX_WEDGES and at most
 // BF_WARP_MAX_SLOTS slots; CTA medium tier for w <= BF_MEDIUM_MAX_WEDGES; CTA
 // heavy tier above.  The kernels' shared-memory layouts are sized from these.
+#ifndef BF_WARP_MAX_WEDGES
 #define BF_WARP_MAX_WEDGES 512u
+#endif
 #define BF_WARP_MAX_SLOTS 32u
+#ifndef BF_MEDIUM_MAX_WEDGES
 #define BF_MEDIUM_MAX_WEDGES 2048u
+#endif
 #define BF_MEDIUM_MAX_SLOTS 128u
 // split starts: at most this many (largest first); row memory per batch
 constexpr uint32_t kMaxSplit = 4096;
