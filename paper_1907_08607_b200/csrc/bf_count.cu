@@ -976,7 +976,7 @@ using MedSM = SmallSmem<MED_CFG>;
 #define BF_BIG_NT 256
 #endif
 #ifndef BF_BIG_CAP
-#define BF_BIG_CAP 8192
+#define BF_BIG_CAP 32768
 #endif
 #ifndef BF_BIG_LCAP
 #define BF_BIG_LCAP 4096
@@ -984,7 +984,10 @@ using MedSM = SmallSmem<MED_CFG>;
 #ifndef BF_BIG_P
 #define BF_BIG_P 32
 #endif
-#define BIG_CFG BF_BIG_NT, BF_BIG_WIN, BF_BIG_CAP, BF_BIG_LCAP, BF_BIG_P, 4, 1
+#ifndef BF_BIG_UR
+#define BF_BIG_UR 2
+#endif
+#define BIG_CFG BF_BIG_NT, BF_BIG_WIN, BF_BIG_CAP, BF_BIG_LCAP, BF_BIG_P, 4, BF_BIG_UR
 constexpr uint64_t HV_WIN_KEYS = BF_BIG_WIN;  // BIG_CFG's window
 using BigSM = HeavySmemT<BIG_CFG>;
 static_assert(BF_WARP_MAX_SLOTS == 32 && BF_MEDIUM_MAX_SLOTS == 128, "tier slot bounds = CTA sizes");
