@@ -24,8 +24,10 @@ if not os.path.exists(LIB_PATH):
 _lib = ctypes.CDLL(LIB_PATH)
 
 BF_OK, BF_EINVAL, BF_ERANGE, BF_EDUP, BF_ENOMEM, BF_ECUDA, BF_ENCCL, BF_ENORANK, BF_EOVERFLOW = range(9)
-BF_RANK_SIDE, BF_RANK_APPROX_DEGREE, BF_RANK_DEGREE = 0, 1, 2
-RANK_KINDS = {"side": BF_RANK_SIDE, "approx_degree": BF_RANK_APPROX_DEGREE, "degree": BF_RANK_DEGREE}
+BF_RANK_SIDE, BF_RANK_APPROX_DEGREE, BF_RANK_DEGREE, BF_RANK_AUTO = 0, 1, 2, 3
+RANK_KINDS = {"side": BF_RANK_SIDE, "approx_degree": BF_RANK_APPROX_DEGREE, "degree": BF_RANK_DEGREE,
+              "auto": BF_RANK_AUTO}
+RANK_NAMES = {v: k for k, v in RANK_KINDS.items()}
 BF_ORIENT_AUTO, BF_ORIENT_LOW, BF_ORIENT_HIGH = 0, 1, 2
 ORIENTS = {"auto": BF_ORIENT_AUTO, "low": BF_ORIENT_LOW, "high": BF_ORIENT_HIGH}
 BF_FLAG_FORCE_WARP, BF_FLAG_FORCE_CTA, BF_FLAG_SMALL_WINDOW, BF_FLAG_FORCE_DENSE = 0x1, 0x2, 0x4, 0x10
@@ -51,6 +53,7 @@ _sig = {
     "bf_count_edge": (ctypes.c_int, [_vp, _vp, _vp]),
     "bf_wedge_count": (ctypes.c_int, [_vp, _u64p]),
     "bf_last_stats": (ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_float), _u64p]),
+    "bf_rank_info": (ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_int), _u64p]),
     "bf_launch_count": (ctypes.c_uint64, [_vp]),
     "bf_deal_index": (ctypes.c_uint64, [ctypes.c_uint64, ctypes.c_int, ctypes.c_int, ctypes.c_uint64,
                                         ctypes.c_uint64]),
@@ -141,6 +144,14 @@ def bf_wedge_count(g) -> int:
     return int(w.value)
 
 
+def bf_rank_info(g):
+    """(ranking in effect, [w_side, w_approx_degree, w_degree]) -- the w's only after BF_RANK_AUTO."""
+    k = ctypes.c_int(0)
+    w = (ctypes.c_uint64 * 3)()
+    _check(_lib.bf_rank_info(g, ctypes.byref(k), w), "bf_rank_info")
+    return RANK_NAMES[k.value], [int(x) for x in w]
+
+
 def bf_last_stats(g):
     """(kernel_ms, call_ms, pairs) of the last bf_count_* on g."""
     a, b, p = ctypes.c_float(0), ctypes.c_float(0), ctypes.c_uint64(0)
@@ -225,6 +236,9 @@ class ButterflyGraph:
 
     def wedges(self) -> int:
         return bf_wedge_count(self.h)
+
+    def rank_info(self):
+        return bf_rank_info(self.h)
 
     def export_csr(self):
         return bf_export_csr(self.h, self.n_u + self.n_v, self.m)

@@ -118,6 +118,46 @@ __global__ void k_rid_maps(const uint32_t* __restrict__ gid_of_rid, uint64_t n, 
   }
 }
 
+// ---- a2 (auto): the paper's f metric ---------------------------
+// W under degree and approximate-degree order without ranking the graph: with
+// k_y = #neighbours of y ranked before y, W = sum_y (k_y d_y - k_y (k_y+1)/2)
+// (App. B of SURVEY; the same closed form the oracle pins).  One pass over the
+// edges decides, per edge, which endpoint is ranked first under each order.
+__device__ __forceinline__ uint64_t rank_key(uint32_t d, uint64_t gid, int approx) {
+  const uint32_t tier = approx ? (d ? 63u - (31u - __clz(d)) : 64u) : 0x7FFFFFFFu - d;
+  return ((uint64_t)tier << 32) | gid;
+}
+
+__global__ void k_auto_k(const uint32_t* __restrict__ e, uint64_t m, uint32_t nU, const uint32_t* __restrict__ deg,
+                         uint32_t* __restrict__ k_deg, uint32_t* __restrict__ k_adeg) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint2 uv = reinterpret_cast<const uint2*>(e)[i];
+    const uint64_t gu = uv.x, gv = (uint64_t)nU + uv.y;
+    const uint32_t du = deg[gu], dv = deg[gv];
+    // the endpoint ranked first is the neighbour "ranked before" the other (its centre)
+    atomicAdd(&k_deg[rank_key(du, gu, 0) < rank_key(dv, gv, 0) ? gv : gu], 1u);
+    atomicAdd(&k_adeg[rank_key(du, gu, 1) < rank_key(dv, gv, 1) ? gv : gu], 1u);
+  }
+}
+
+__global__ void k_auto_w(const uint32_t* __restrict__ deg, const uint32_t* __restrict__ k_deg,
+                         const uint32_t* __restrict__ k_adeg, uint64_t n, unsigned long long* __restrict__ w) {
+  __shared__ unsigned long long s[2];
+  if (threadIdx.x < 2) s[threadIdx.x] = 0;
+  __syncthreads();
+  unsigned long long a = 0, b = 0;
+  for (uint64_t z = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; z < n; z += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t d = deg[z], k1 = k_deg[z], k2 = k_adeg[z];
+    a += k1 * d - k1 * (k1 + 1) / 2;
+    b += k2 * d - k2 * (k2 + 1) / 2;
+  }
+  a = warp_sum(a);
+  b = warp_sum(b);
+  if ((threadIdx.x & 31) == 0) { atomicAdd(&s[0], a); atomicAdd(&s[1], b); }
+  __syncthreads();
+  if (threadIdx.x < 2) atomicAdd(&w[threadIdx.x], s[threadIdx.x]);
+}
+
 // ---- a3 -----------------------------------------------------------------------
 __global__ void k_slot_keys(const uint32_t* __restrict__ e, uint64_t m, uint32_t nU, uint64_t n, int B,
                             const uint32_t* __restrict__ rid_of_gid, uint64_t* __restrict__ keys,
@@ -315,8 +355,55 @@ bf_status graph_ingest(bf_graph* g, const uint32_t* edges) {
   return BF_OK;
 }
 
+// BF_RANK_AUTO: side order if f = (w_s - w_r) / w_s < 0.1, else the one of
+// degree / approximate-degree order with fewer wedges
+static bf_status rank_auto(bf_graph* g, int* kind) {
+  cudaStream_t s = g->stream;
+  const uint64_t n = g->n, m = g->m, n1 = std::max<uint64_t>(n, 1);
+  g->tmp_c.ensure(n1 * 4 + 64);
+  g->tmp_d.ensure(n1 * 4 + 64);
+  g->tmp_b.ensure(64);
+  uint32_t* kd = g->tmp_c.as<uint32_t>();
+  uint32_t* ka = g->tmp_d.as<uint32_t>();
+  unsigned long long* w = g->tmp_b.as<unsigned long long>();  // [0] degree, [1] approx, [2..3] side sums
+  CUDA_TRY(cudaMemsetAsync(kd, 0, n1 * 4, s));
+  CUDA_TRY(cudaMemsetAsync(ka, 0, n1 * 4, s));
+  CUDA_TRY(cudaMemsetAsync(w, 0, 32, s));
+  if (n) {
+    k_side_sums<<<grid_for(n, g->sms), TPB, 0, s>>>(g->deg.as<uint32_t>(), n, g->n_u, w + 2);
+    KERNEL_CHECK(g);
+  }
+  if (m) {
+    k_auto_k<<<grid_for(m, g->sms), TPB, 0, s>>>(g->edges.as<uint32_t>(), m, g->n_u, g->deg.as<uint32_t>(), kd, ka);
+    KERNEL_CHECK(g);
+  }
+  if (n) {
+    k_auto_w<<<grid_for(n, g->sms), TPB, 0, s>>>(g->deg.as<uint32_t>(), kd, ka, n, w);
+    KERNEL_CHECK(g);
+  }
+  unsigned long long h[4];
+  CUDA_TRY(cudaMemcpyAsync(h, w, 32, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  const uint64_t w_side = std::min<uint64_t>(h[2], h[3]);  // reading Z1: the cheaper side as endpoints
+  const uint64_t w_deg = h[0], w_adeg = h[1];
+  const uint64_t w_r = std::min(w_deg, w_adeg);
+  g->w_auto[0] = w_side;
+  g->w_auto[1] = w_adeg;
+  g->w_auto[2] = w_deg;
+  // f < 0.1  <=>  10 (w_s - w_r) < w_s (integer arithmetic; f <= 0 when w_r >= w_s)
+  const bool side = w_r >= w_side || (unsigned __int128)10 * (w_side - w_r) < (unsigned __int128)w_side;
+  *kind = side ? BF_RANK_SIDE : (w_deg <= w_adeg ? BF_RANK_DEGREE : BF_RANK_APPROX_DEGREE);
+  return BF_OK;
+}
+
 bf_status graph_rank(bf_graph* g, int kind) {
   cudaStream_t s = g->stream;
+  if (kind == BF_RANK_AUTO) {
+    bf_status st = rank_auto(g, &kind);
+    if (st != BF_OK) return st;
+  } else {
+    g->w_auto[0] = g->w_auto[1] = g->w_auto[2] = 0;
+  }
   const uint64_t n = g->n, m = g->m, S = 2 * m;
   const uint64_t n1 = std::max<uint64_t>(n, 1), S1 = std::max<uint64_t>(S, 1);
   g->rid_of_gid.ensure(n1 * 4);

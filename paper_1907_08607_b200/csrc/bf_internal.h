@@ -105,7 +105,8 @@ struct bf_graph {
 
   // a2/a3: ranking and ranked CSR (rid space)
   bool ranked = false;
-  int rank_kind = -1;
+  int rank_kind = -1;       // the ranking in effect (BF_RANK_AUTO resolves to one of the others)
+  uint64_t w_auto[3] = {0, 0, 0};  // BF_RANK_AUTO: W under side, approximate-degree, degree order
   int orient = BF_ORIENT_HIGH;
   DevBuf rid_of_gid;  // u32 [n]
   DevBuf gid_of_rid;  // u32 [n]

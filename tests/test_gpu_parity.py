@@ -229,3 +229,24 @@ def test_repeated_graphs_same_process(bf, orient):
                 bu, bv_, t = bg.vertex()
                 assert t == ref["total"] and np.array_equal(bu, ref["b_u"]) and np.array_equal(bv_, ref["b_v"])
                 assert bg.total() == ref["total"], (rep, flags)
+
+
+@pytest.mark.parametrize("k,scale", [(1, 1.0), (2, 0.02), (3, 0.01), (4, 0.01), (5, 0.004)])
+def test_rank_auto_f_metric(bf, k, scale):
+    """BF_RANK_AUTO: the wedge counts of the three candidate orders
+    computed before ranking equal the oracle's W for each order; the choice
+    follows f = (w_s - w_r)/w_s < 0.1 -> side; the counts stay exact."""
+    g = bfgen.config_graph(k, scale)
+    with oracle.OracleGraph(g.n_u, g.n_v, g.edges) as og:
+        W = {kind: og.wedges(og.rank(kind))[0] for kind in ("side", "approx_degree", "degree")}
+    ref = oracle.count(g.n_u, g.n_v, g.edges, edge=False)
+    with bf.ButterflyGraph(g.n_u, g.n_v, g.edges, rank="auto") as bg:
+        kind, w = bg.rank_info()
+        assert w == [W["side"], W["approx_degree"], W["degree"]]
+        wr = min(W["degree"], W["approx_degree"])
+        side = wr >= W["side"] or 10 * (W["side"] - wr) < W["side"]
+        expect = "side" if side else ("degree" if W["degree"] <= W["approx_degree"] else "approx_degree")
+        assert kind == expect
+        assert bg.wedges() == W[kind]
+        bu, bv, t = bg.vertex()
+        assert t == ref["total"] and np.array_equal(bu, ref["b_u"]) and np.array_equal(bv, ref["b_v"])
