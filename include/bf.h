@@ -183,6 +183,27 @@ bf_status bf_nccl_unique_id(uint8_t id[128]);
 bf_status bf_nccl_comm_create(const uint8_t id[128], int rank, int world, int device, void** comm);
 bf_status bf_nccl_comm_destroy(void* comm);
 
+/* Approximate total counting by sparsification (§4.4, P:1451-1493;
+ * Sanei-Mehri et al.): filters the edge list on the device and writes the kept
+ * edges, in input order, to out_edges (capacity m pairs; host unless
+ * opt->outputs_on_device) and their number to *out_m.  The caller counts the
+ * sparsified graph exactly (bf_graph_create .. bf_count_total, total counts
+ * only) and scales the count into an unbiased estimate of T:
+ *   BF_SPARSIFY_EDGE   keep edge e iff h(seed, e) < p * 2^64 (each edge with
+ *                      probability p)            -> T_s / p^4
+ *   BF_SPARSIFY_COLOR  colour(z) = h(seed ^ 0xD1B54A32D192ED03, gid z) mod c,
+ *                      c = ceil(1/p); keep an edge iff its endpoints share a
+ *                      colour                    -> T_s * c^3
+ * h(s, x) = splitmix64 finalizer of s + (x+1) * 0x9E3779B97F4A7C15 (counter
+ * based: results depend only on (seed, index)).  edges: m pairs (u, v), host
+ * unless opt->edges_on_device; opt may be NULL; ids are not range-checked here
+ * (bf_graph_create checks the output).  Errors: BF_EINVAL (NULL pointers, p not
+ * in (0,1], bad method, m >= 2^31), BF_ENOMEM, BF_ECUDA. */
+#define BF_SPARSIFY_EDGE 0
+#define BF_SPARSIFY_COLOR 1
+bf_status bf_sparsify(uint32_t n_u, uint32_t n_v, const uint32_t* edges, uint64_t m, int method, double p,
+                      uint64_t seed, uint32_t* out_edges, uint64_t* out_m, const bf_options* opt);
+
 /* Frees all device state of g (NULL is a no-op). */
 void bf_graph_destroy(bf_graph* g);
 

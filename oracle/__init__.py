@@ -15,6 +15,7 @@ the wedge-count closed form.  No oracle function is "parity unpinned".
 from __future__ import annotations
 
 import ctypes
+import math
 import os
 import subprocess
 
@@ -55,6 +56,10 @@ def _load():
         lib.orc_edge.argtypes = [vp, u32p, ctypes.c_uint64, u64p]
         lib.orc_rank.argtypes = [vp, ctypes.c_int, u32p]
         lib.orc_wedges.argtypes = [vp, u32p, u64p, u64p]
+        lib.orc_h64.argtypes = [ctypes.c_uint64, ctypes.c_uint64]
+        lib.orc_h64.restype = ctypes.c_uint64
+        lib.orc_sparsify.argtypes = [ctypes.c_uint32, u32p, ctypes.c_uint64, ctypes.c_int, ctypes.c_uint64,
+                                     ctypes.c_int, ctypes.c_uint32, ctypes.c_uint64, vp]
         _lib = lib
     return _lib
 
@@ -170,3 +175,24 @@ class OracleGraph:
 def count(n_u, n_v, edges, **kw):
     with OracleGraph(n_u, n_v, edges) as g:
         return g.count(**kw)
+
+
+def h64(seed: int, x: int) -> int:
+    """The sparsifiers' counter-based hash (splitmix64 step of seed + (x+1)*golden)."""
+    _load()
+    return int(_lib.orc_h64(ctypes.c_uint64(seed & (2**64 - 1)), ctypes.c_uint64(x)))
+
+
+def sparsify(n_u: int, edges: np.ndarray, method: str, p: float, seed: int) -> np.ndarray:
+    """Edge / colorful sparsification (PAPER.md 4.4): the kept edges
+    in input order.  Edge: keep e iff h(seed, e) < p*2^64; colour: c = ceil(1/p)
+    colours by h(seed ^ salt, gid), keep iff the endpoints share a colour."""
+    lib = _load()
+    e = np.ascontiguousarray(edges, dtype=np.uint32).reshape(-1, 2)
+    keep = np.zeros(max(len(e), 1), np.uint8)
+    keep_all = int(p >= 1.0)
+    thr = 2**64 - 1 if keep_all else int(math.ldexp(p, 64))
+    colors = int(math.ceil(1.0 / p))
+    _check(lib.orc_sparsify(n_u, _p32(e), len(e), {"edge": 0, "color": 1}[method], ctypes.c_uint64(thr), keep_all,
+                            colors, ctypes.c_uint64(seed & (2**64 - 1)), keep.ctypes.data_as(ctypes.c_void_p)))
+    return e[keep[:len(e)].astype(bool)]

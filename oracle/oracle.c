@@ -286,3 +286,38 @@ int orc_wedges(const orc_graph* g, const uint32_t* rank, uint64_t* w_out, uint64
   *total = (uint64_t)W;
   return ORC_OK;
 }
+
+/* ------------------------------------------------------------------------
+ * Sparsification (§4.4), written out from the
+ * definition for the approximate-counting pins; the counter-based generator
+ * is the published splitmix64 step, restated here (not shared with the CUDA
+ * path): h(s, x) = mix(s + (x+1)*0x9E3779B97F4A7C15).
+ *   method 0 (edge):   keep edge e iff h(seed, e) < p*2^64 (keep_all: p = 1)
+ *   method 1 (colour): colour(z) = h(seed ^ 0xD1B54A32D192ED03, gid z) mod c;
+ *                      keep an edge iff both endpoints have the same colour
+ * keep[e] receives 0/1.
+ */
+static uint64_t splitmix_out(uint64_t state) {
+  uint64_t z = state;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+uint64_t orc_h64(uint64_t seed, uint64_t x) { return splitmix_out(seed + (x + 1) * 0x9E3779B97F4A7C15ull); }
+
+int orc_sparsify(uint32_t nU, const uint32_t* edges, uint64_t m, int method, uint64_t thr, int keep_all,
+                 uint32_t colors, uint64_t seed, uint8_t* keep) {
+  if (method != 0 && method != 1) return ORC_EINVAL;
+  if (method == 1 && colors == 0) return ORC_EINVAL;
+  for (uint64_t e = 0; e < m; e++) {
+    if (method == 0) {
+      keep[e] = keep_all || orc_h64(seed, e) < thr;
+    } else {
+      uint64_t s2 = seed ^ 0xD1B54A32D192ED03ull;
+      uint64_t cu = orc_h64(s2, edges[2 * e]) % colors;
+      uint64_t cv = orc_h64(s2, (uint64_t)nU + edges[2 * e + 1]) % colors;
+      keep[e] = cu == cv;
+    }
+  }
+  return ORC_OK;
+}

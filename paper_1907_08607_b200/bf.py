@@ -54,6 +54,8 @@ _sig = {
     "bf_wedge_count": (ctypes.c_int, [_vp, _u64p]),
     "bf_last_stats": (ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_float), _u64p]),
     "bf_rank_info": (ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_int), _u64p]),
+    "bf_sparsify": (ctypes.c_int, [ctypes.c_uint32, ctypes.c_uint32, _vp, ctypes.c_uint64, ctypes.c_int,
+                                   ctypes.c_double, ctypes.c_uint64, _vp, _u64p, ctypes.POINTER(bf_options)]),
     "bf_launch_count": (ctypes.c_uint64, [_vp]),
     "bf_deal_index": (ctypes.c_uint64, [ctypes.c_uint64, ctypes.c_int, ctypes.c_int, ctypes.c_uint64,
                                         ctypes.c_uint64]),
@@ -150,6 +152,34 @@ def bf_rank_info(g):
     w = (ctypes.c_uint64 * 3)()
     _check(_lib.bf_rank_info(g, ctypes.byref(k), w), "bf_rank_info")
     return RANK_NAMES[k.value], [int(x) for x in w]
+
+
+BF_SPARSIFY_EDGE, BF_SPARSIFY_COLOR = 0, 1
+SPARSIFY_METHODS = {"edge": BF_SPARSIFY_EDGE, "color": BF_SPARSIFY_COLOR}
+
+
+def bf_sparsify(n_u: int, n_v: int, edges, method, p: float, seed: int, opt: bf_options | None = None):
+    """Device edge filter of approximate counting.  Host numpy in,
+    host numpy out (the kept edges in input order)."""
+    o = opt if opt is not None else bf_options_default()
+    e = np.ascontiguousarray(edges, dtype=np.uint32).reshape(-1, 2)
+    out = np.zeros((max(e.shape[0], 1), 2), np.uint32)
+    k = ctypes.c_uint64(0)
+    mth = SPARSIFY_METHODS[method] if isinstance(method, str) else int(method)
+    _check(_lib.bf_sparsify(n_u, n_v, _ptr(e), e.shape[0], mth, float(p), int(seed) & (2**64 - 1), _ptr(out),
+                            ctypes.byref(k), ctypes.byref(o)), "bf_sparsify")
+    return out[:int(k.value)]
+
+
+def approx_total(n_u: int, n_v: int, edges, p: float, method="edge", seed: int = 0, rank="auto", **opts) -> float:
+    """Unbiased estimate of the total butterfly count: sparsify on the device,
+    count the kept graph exactly, scale by p^-4 (edge) or ceil(1/p)^3 (colour)."""
+    kept = bf_sparsify(n_u, n_v, edges, method, p, seed)
+    with ButterflyGraph(n_u, n_v, kept, rank=rank, **opts) as bg:
+        t = bg.total()
+    if (SPARSIFY_METHODS[method] if isinstance(method, str) else int(method)) == BF_SPARSIFY_EDGE:
+        return t / p ** 4
+    return t * float(np.ceil(1.0 / p)) ** 3
 
 
 def bf_last_stats(g):

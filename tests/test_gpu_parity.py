@@ -250,3 +250,23 @@ def test_rank_auto_f_metric(bf, k, scale):
         assert bg.wedges() == W[kind]
         bu, bv, t = bg.vertex()
         assert t == ref["total"] and np.array_equal(bu, ref["b_u"]) and np.array_equal(bv, ref["b_v"])
+
+
+@pytest.mark.parametrize("method", ["edge", "color"])
+@pytest.mark.parametrize("p", [1.0, 0.5, 0.2])
+def test_sparsify_matches_oracle(bf, method, p):
+    """Approximate counting: the device filter keeps exactly the
+    oracle's edges (same counter-based hash, implemented on both sides), the
+    sparsified graph's count is exact, and p = 1 reproduces T."""
+    g = bfgen.config_graph(2, 0.01)
+    for seed in (1, 77):
+        kept = bf.bf_sparsify(g.n_u, g.n_v, g.edges, method, p, seed)
+        ref_kept = oracle.sparsify(g.n_u, g.edges, method, p, seed)
+        assert np.array_equal(kept, ref_kept), (method, p, seed)
+        ref = oracle.count(g.n_u, g.n_v, ref_kept, vertex=False, edge=False)["total"] if len(ref_kept) else 0
+        est = bf.approx_total(g.n_u, g.n_v, g.edges, p, method=method, seed=seed)
+        scale = p ** -4 if method == "edge" else float(np.ceil(1.0 / p)) ** 3
+        assert est == ref * scale
+    if p == 1.0:
+        T = oracle.count(g.n_u, g.n_v, g.edges, vertex=False, edge=False)["total"]
+        assert bf.approx_total(g.n_u, g.n_v, g.edges, 1.0, method=method) == T
