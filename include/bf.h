@@ -110,20 +110,22 @@ typedef struct {
 /* Fills *opt with defaults: device 0, library stream, 1 GPU, host pointers. */
 void bf_options_default(bf_options* opt);
 
-/* Copies the edge list to the device, range-checks it, rejects duplicates and
- * computes degrees (§8(a) a1).  edges: m pairs (u, v), uint32, row-major
+/* Copies the edge list to the device, range-checks it and computes degrees
+ * (§8(a) a1).  Repeated (u,v) pairs are rejected by bf_rank, where the ranked
+ * slot sort makes them adjacent (no separate hash pass).  edges: m pairs (u, v), uint32, row-major
  * [m][2]; host pointer unless opt->edges_on_device.  The caller keeps
  * ownership of `edges` and may free it after the call returns.
  * opt may be NULL (defaults).  *out receives the graph (NULL on error).
- * Errors: BF_EINVAL (NULL out, size over limit), BF_ERANGE, BF_EDUP,
- * BF_ENOMEM, BF_ECUDA. */
+ * Errors: BF_EINVAL (NULL out, size over limit), BF_ERANGE, BF_ENOMEM,
+ * BF_ECUDA. */
 bf_status bf_graph_create(uint32_t n_u, uint32_t n_v, const uint32_t* edges, uint64_t m,
                           const bf_options* opt, bf_graph** out);
 
 /* Ranks the vertices (§8(a) a2), builds the ranked CSR of Alg. 1 (a3) and
  * the per-start wedge counts and work plan (a4).  Deterministic and identical
  * on every rank.  May be called again to re-rank.  Errors: BF_EINVAL (bad
- * kind / NULL g), BF_ENOMEM, BF_ECUDA. */
+ * kind / NULL g), BF_EDUP (a (u,v) pair occurs twice: the graph must be
+ * simple, reading Z8), BF_ENOMEM, BF_ECUDA. */
 bf_status bf_rank(bf_graph* g, bf_rank_kind kind);
 
 /* Global butterfly count (P:487 footnote: Σ over endpoint pairs of C(d,2)).

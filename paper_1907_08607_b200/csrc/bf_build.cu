@@ -53,23 +53,6 @@ __global__ void k_validate_degree(const uint32_t* __restrict__ e, uint64_t m, ui
   }
 }
 
-// open-addressing set of keys u*nV+v+1 (0 = empty); a repeated key sets flag 2
-__global__ void k_dup_check(const uint32_t* __restrict__ e, uint64_t m, uint32_t nV,
-                            unsigned long long* __restrict__ table, uint64_t mask, uint32_t* __restrict__ flags) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
-    uint2 uv = reinterpret_cast<const uint2*>(e)[i];
-    unsigned long long key = (unsigned long long)uv.x * nV + uv.y + 1ull;
-    unsigned long long h = (key * 0x9E3779B97F4A7C15ull) >> 17;
-    for (;;) {
-      h &= mask;
-      unsigned long long old = atomicCAS(&table[h], 0ull, key);
-      if (old == 0ull) break;
-      if (old == key) { atomicOr(flags, 2u); break; }
-      h++;
-    }
-  }
-}
-
 // ---- a2 -----------------------------------------------------------------------
 __global__ void k_side_sums(const uint32_t* __restrict__ deg, uint64_t n, uint32_t nU,
                             unsigned long long* __restrict__ sums /*[2]: wedges with U / V endpoints*/) {
@@ -185,12 +168,15 @@ __global__ void k_slot_decode(const uint64_t* __restrict__ keys, const uint32_t*
   }
 }
 
+// also rejects repeated edges: after the slot sort a repeated (u,v) pair is
+// two adjacent equal slots of the same source (reading Z8)
 __global__ void k_pos_hi(const uint32_t* __restrict__ vals, const uint32_t* __restrict__ where,
                          const uint32_t* __restrict__ nbr, const uint32_t* __restrict__ src,
                          const uint32_t* __restrict__ off, const uint64_t* __restrict__ rkey, uint64_t S,
-                         uint32_t* __restrict__ pos, uint32_t* __restrict__ hi) {
+                         uint32_t* __restrict__ pos, uint32_t* __restrict__ hi, uint32_t* __restrict__ flags) {
   for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < S; j += (uint64_t)gridDim.x * blockDim.x) {
     uint32_t y = nbr[j], x = src[j];
+    if (j + 1 < off[x + 1] && nbr[j + 1] == y) atomicOr(flags, 2u);
     uint32_t twin = where[vals[j] ^ 1u];
     pos[j] = twin - off[y];
     bool f = rkey[y] > rkey[x];
@@ -339,19 +325,11 @@ bf_status graph_ingest(bf_graph* g, const uint32_t* edges) {
     k_validate_degree<<<grid_for(m, g->sms), TPB, 0, s>>>(g->edges.as<uint32_t>(), m, g->n_u, g->n_v,
                                                           g->deg.as<uint32_t>(), flags);
     KERNEL_CHECK(g);
-    uint64_t cap = 1;
-    while (cap < 2 * m) cap <<= 1;
-    g->tmp_b.ensure(cap * 8);
-    CUDA_TRY(cudaMemsetAsync(g->tmp_b.p, 0, cap * 8, s));
-    k_dup_check<<<grid_for(m, g->sms), TPB, 0, s>>>(g->edges.as<uint32_t>(), m, g->n_v,
-                                                    g->tmp_b.as<unsigned long long>(), cap - 1, flags);
-    KERNEL_CHECK(g);
   }
   uint32_t hflags = 0;
   CUDA_TRY(cudaMemcpyAsync(&hflags, flags, 4, cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaStreamSynchronize(s));
   if (hflags & 1u) { bf_set_error("edge id out of range"); return BF_ERANGE; }
-  if (hflags & 2u) { bf_set_error("duplicate edge"); return BF_EDUP; }
   return BF_OK;
 }
 
@@ -462,6 +440,8 @@ bf_status graph_rank(bf_graph* g, int kind) {
   uint32_t* v0 = g->tmp_c.as<uint32_t>();
   uint32_t* v1 = g->tmp_d.as<uint32_t>();
   CUDA_TRY(cudaMemsetAsync(g->hi.p, 0, n1 * 4, s));
+  g->dflag.ensure(16);
+  CUDA_TRY(cudaMemsetAsync(g->dflag.p, 0, 4, s));
   if (m) {
     k_slot_keys<<<grid_for(m, g->sms), TPB, 0, s>>>(g->edges.as<uint32_t>(), m, g->n_u, n, B,
                                                      g->rid_of_gid.as<uint32_t>(), k0, v0);
@@ -475,7 +455,7 @@ bf_status graph_rank(bf_graph* g, int kind) {
     KERNEL_CHECK(g);
     k_pos_hi<<<grid_for(S, g->sms), TPB, 0, s>>>(vs, where, g->nbr.as<uint32_t>(), src, g->off.as<uint32_t>(),
                                                   g->rkey.as<uint64_t>(), S, g->pos.as<uint32_t>(),
-                                                  g->hi.as<uint32_t>());
+                                                  g->hi.as<uint32_t>(), g->dflag.as<uint32_t>());
     KERNEL_CHECK(g);
   }
   g->rank_kind = kind;
@@ -542,10 +522,12 @@ bf_status graph_plan(bf_graph* g) {
     KERNEL_CHECK(g);
   }
   uint64_t host = 0;
-  uint32_t hc[3];
+  uint32_t hc[3], hflag = 0;
   CUDA_TRY(cudaMemcpyAsync(&host, dW, 8, cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaMemcpyAsync(hc, cnts, 12, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaMemcpyAsync(&hflag, g->dflag.p, 4, cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaStreamSynchronize(s));
+  if (hflag & 2u) { bf_set_error("duplicate edge"); return BF_EDUP; }
   g->W = host;
   const uint32_t nnz = hc[0];
   g->n_tier[0] = hc[1];

@@ -157,6 +157,7 @@ struct bf_graph {
   DevBuf otouch;  // u32 per-CTA global touched lists (multi-chunk starts)
   DevBuf queue;   // u32 [4] work-queue counters
   DevBuf hub;     // u64 striped endpoint sums of hub keys (vertex mode)
+  DevBuf dflag;   // u32 duplicate-edge flag of the ranked slot sort
 
   // temp for primitives
   DevBuf tmp_a, tmp_b, tmp_c, tmp_d, tmp_e, tmp_f, tmp_scan;
@@ -167,7 +168,7 @@ struct bf_graph {
 
   template <class F> void for_each_buf(F f) {
     DevBuf* bufs[] = {&edges, &deg, &rid_of_gid, &gid_of_rid, &rkey, &off, &nbr, &pos, &hi, &where,
-                      &wstart, &seglo, &seglen, &wpre, &items, &order, &bv, &acc, &be, &total, &orow, &otouch, &queue, &hub, &split, &split_off, &split_cnt, &pieces, &srow, &slist,
+                      &wstart, &seglo, &seglen, &wpre, &items, &order, &bv, &acc, &be, &total, &orow, &otouch, &queue, &hub, &dflag, &split, &split_off, &split_cnt, &pieces, &srow, &slist,
                       &tmp_a, &tmp_b, &tmp_c, &tmp_d, &tmp_e, &tmp_f, &tmp_scan};
     for (DevBuf* b : bufs) f(*b);
   }

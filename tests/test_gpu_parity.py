@@ -270,3 +270,15 @@ def test_sparsify_matches_oracle(bf, method, p):
     if p == 1.0:
         T = oracle.count(g.n_u, g.n_v, g.edges, vertex=False, edge=False)["total"]
         assert bf.approx_total(g.n_u, g.n_v, g.edges, 1.0, method=method) == T
+
+
+def test_duplicate_in_large_graph(bf):
+    """Reading Z8: a single repeated pair anywhere in the list is rejected (by
+    bf_rank: the ranked slot sort makes the two copies adjacent)."""
+    g = bfgen.chung_lu(3000, 2000, 30000, 2.1, 2.2, seed=7)
+    for pick in (0, 12345, g.m - 1):
+        e = np.concatenate([g.edges, g.edges[pick:pick + 1]])
+        e = e[np.random.default_rng(pick).permutation(len(e))]
+        with pytest.raises(bf.BFError) as ei:
+            bf.ButterflyGraph(g.n_u, g.n_v, e)
+        assert ei.value.status == bf.BF_EDUP
