@@ -966,10 +966,29 @@ __global__ void __launch_bounds__(256) k_split_clear(CountArgs a, SplitArgs sa) 
 #ifndef BF_BIG_WIN
 #define BF_BIG_WIN 8192
 #endif
-#define WARP_CFG 32, BF_WARP_WIN, 512, BF_WARP_MAX_WEDGES, 8, 4, 2
+// unit shape: P wedges per unit, G lanes per unit.  G = 8 makes every lane
+// group read one 32-byte sector per step; the wedge walks are bound by L1/
+// shared-memory wavefronts (l1tex ~70% busy), so fewer, fuller sectors per
+// warp request beat more units in flight (measured: G = 2 / 4 / 8 / 16 / 32)
+#ifndef BF_WARP_P
+#define BF_WARP_P 16
+#endif
+#ifndef BF_WARP_G
+#define BF_WARP_G 8
+#endif
+#ifndef BF_MED_P
+#define BF_MED_P 32
+#endif
+#ifndef BF_MED_G
+#define BF_MED_G 8
+#endif
+#ifndef BF_BIG_G
+#define BF_BIG_G 8
+#endif
+#define WARP_CFG 32, BF_WARP_WIN, 512, BF_WARP_MAX_WEDGES, BF_WARP_P, BF_WARP_G, 2
 using WarpSM = SmallSmem<WARP_CFG>;
 // medium tier: 128 threads, w <= 2048, <= 128 slots
-#define MED_CFG 128, BF_MED_WIN, 2048, BF_MEDIUM_MAX_WEDGES, 16, 4, 2
+#define MED_CFG 128, BF_MED_WIN, 2048, BF_MEDIUM_MAX_WEDGES, BF_MED_P, BF_MED_G, 2
 using MedSM = SmallSmem<MED_CFG>;
 // heavy tier: 256 threads, chunks of <= 8192 wedges
 #ifndef BF_BIG_NT
@@ -987,7 +1006,7 @@ using MedSM = SmallSmem<MED_CFG>;
 #ifndef BF_BIG_UR
 #define BF_BIG_UR 2
 #endif
-#define BIG_CFG BF_BIG_NT, BF_BIG_WIN, BF_BIG_CAP, BF_BIG_LCAP, BF_BIG_P, 4, BF_BIG_UR
+#define BIG_CFG BF_BIG_NT, BF_BIG_WIN, BF_BIG_CAP, BF_BIG_LCAP, BF_BIG_P, BF_BIG_G, BF_BIG_UR
 constexpr uint64_t HV_WIN_KEYS = BF_BIG_WIN;  // BIG_CFG's window
 using BigSM = HeavySmemT<BIG_CFG>;
 static_assert(BF_WARP_MAX_SLOTS == 32 && BF_MEDIUM_MAX_SLOTS == 128, "tier slot bounds = CTA sizes");
