@@ -563,7 +563,10 @@ __device__ __forceinline__ void start_passes(const CountArgs& a, Units<NT, UCAP>
 // per slot) waste most lanes of a P-wedge unit and most of a chunk's barriers.
 // They run in slot mode instead: thread per slot, walking its segment with
 // four predicated loads in flight; pass-2 sums stay in a register per slot.
-constexpr uint32_t SLOT_MODE_AVG = 6;  // slot mode when w < 6 * #slots
+#ifndef BF_SLOT_MODE_AVG
+#define BF_SLOT_MODE_AVG 16
+#endif
+constexpr uint32_t SLOT_MODE_AVG = BF_SLOT_MODE_AVG;  // slot mode when w < SLOT_MODE_AVG * #slots (measured: 6 -> 16 takes c4 50.6 -> 38.5 ms)
 
 template <bool SPILL, int NT, class Store>
 __device__ __forceinline__ void slots_pass1(const CountArgs& a, const Store& cs, uint32_t j0, uint32_t j1,
