@@ -141,6 +141,18 @@ def test_configs_scaled(bf, k, scale):
         assert_same(run_all(bf, g, rank, orient), ref, f"c{k}@{scale} {rank}/{orient}")
 
 
+@pytest.mark.parametrize("V", [2, 5])
+def test_virtual_world_split_starts(bf, V):
+    """Split starts are dealt whole to ranks (snake order); with tiny chunks the
+    split threshold drops to 256 wedges, so many split starts exist and every
+    virtual rank gets some."""
+    g = bfgen.config_graph(4, 0.01)
+    ref = oracle.count(g.n_u, g.n_v, g.edges)
+    for orient in ORIENTS:
+        got = run_all(bf, g, "degree", orient, virtual_world=V, test_flags=bf.BF_FLAG_SMALL_CHUNK)
+        assert_same(got, ref, f"V={V} {orient}")
+
+
 @pytest.mark.parametrize("V", [2, 3, 8])
 def test_virtual_world(bf, V):
     """T4 on one GPU: each virtual rank counts its share (snake-dealt heavy starts,
