@@ -179,8 +179,7 @@ __device__ __forceinline__ uint64_t* endpoint_slot(const CountArgs& a, uint32_t 
 __device__ __forceinline__ uint32_t hslot(uint32_t key, uint32_t shift) { return (key * 0x9E3779B1u) >> shift; }
 
 struct SmallStore {
-  uint32_t* win;  // u8 counters, four per word (key kk: word kk & w4m, byte kk >> w4s)
-  uint32_t w4m, w4s;
+  uint32_t* win;  // u8 counters, four per word (key kk: byte kk)
   uint32_t* hk;
   uint32_t* hv;   // u8 counts, four per word
   uint32_t wl, hmask, shift;
@@ -188,11 +187,9 @@ struct SmallStore {
   // returns true if this increment took the key's count from 0 to 1
   __device__ __forceinline__ bool add(uint32_t key, uint32_t kk, bool& hashed) const {
     if (kk < wl) {
-      // key kk lives in byte kk >> w4s of word kk & w4m: neighbouring keys (the
-      // hottest hubs are rids 0, 1, 2, ...) never share a word or a bank
-      BF_CHECK(__isShared(win + (kk & w4m)));
-      const uint32_t sh = (kk >> w4s) << 3;
-      const uint32_t old = atomicAdd(win + (kk & w4m), 1u << sh);
+      BF_CHECK(__isShared(win + (kk >> 2)));
+      const uint32_t sh = (kk & 3u) << 3;
+      const uint32_t old = atomicAdd(win + (kk >> 2), 1u << sh);
       return ((old >> sh) & 0xffu) == 0u;
     }
     hashed = true;
@@ -208,7 +205,7 @@ struct SmallStore {
     }
   }
   __device__ __forceinline__ uint32_t get(uint32_t key, uint32_t kk) const {
-    if (kk < wl) return ((const uint8_t*)win)[((kk & w4m) << 2) | (kk >> w4s)];
+    if (kk < wl) return ((const uint8_t*)win)[kk];
     uint32_t h = hslot(key, shift);
     for (uint32_t probes = 0; hk[h] != key; probes++) {
       if (probes > hmask) __trap();  // the key was inserted in pass 1
@@ -220,7 +217,7 @@ struct SmallStore {
   // never strands a lookup: get() probes past EMPTY slots)
   __device__ __forceinline__ void zero(uint32_t key, uint32_t kk) const {
     if (kk < wl) {
-      ((uint8_t*)win)[((kk & w4m) << 2) | (kk >> w4s)] = 0;
+      ((uint8_t*)win)[kk] = 0;
       return;
     }
     uint32_t h = hslot(key, shift);
@@ -395,7 +392,6 @@ __device__ __forceinline__ void units_pass1(const CountArgs& a, Units<NT, UCAP>&
 #pragma unroll
       for (int it = 0; it < IT; it++) {
         uint32_t k = key[r][it];
-        if ((a.exp & 32) && k != EMPTY) k = kbase + (((k - kbase) * 0x9E3779B1u) >> 20);  // timing only: scatter hub keys
         if (k != EMPTY) {
           BF_CHECK(k < a.n);
           if (CACHE) cache[ps[r] + gl + it * G] = k;
@@ -651,8 +647,6 @@ __global__ void __launch_bounds__(NT, 1) k_small(CountArgs a) {
   static_assert((HS & (HS - 1)) == 0 && (WIN & (WIN - 1)) == 0 && WIN >= 4, "store sizes");
   SmallStore cs;
   cs.win = ss.win;
-  cs.w4m = WIN / 4 - 1;
-  cs.w4s = 31 - __clz(WIN / 4);
   cs.hk = ss.hk;
   cs.hv = ss.hv;
   cs.wl = min(a.win, WIN);
