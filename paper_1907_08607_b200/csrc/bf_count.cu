@@ -404,7 +404,9 @@ __device__ __forceinline__ void units_pass1(const CountArgs& a, Units<NT, UCAP>&
 // pass 2 over the chunk's units: c = d(key) - 1 per wedge, summed per slot
 // (centre y in vertex mode, edge (s, y) in edge mode); edge mode also adds c
 // to the wedge's (y, key) edge
-template <int MODE, bool CACHE, int NT, int P, int G, int UR, uint32_t UCAP, class Store>
+// NARROW: the start's d < 2^32 / P (d <= #slots), so a lane group's sum of
+// d-1 fits u32 and the group reduction shuffles 32-bit words
+template <int MODE, bool CACHE, int NT, int P, int G, int UR, uint32_t UCAP, class Store, bool NARROW = true>
 __device__ __forceinline__ void units_pass2(const CountArgs& a, Units<NT, UCAP>& u, const Store& cs,
                                             uint32_t kbase, const uint32_t* cache) {
   constexpr int IT = P / G;
@@ -429,7 +431,7 @@ __device__ __forceinline__ void units_pass2(const CountArgs& a, Units<NT, UCAP>&
 #pragma unroll
     for (int r = 0; r < UR; r++) {
       const uint32_t x = xb + r * NG + (tid & 31) / G;
-      uint64_t s = 0;
+      typename std::conditional<NARROW, uint32_t, uint64_t>::type s = 0;
 #pragma unroll
       for (int it = 0; it < IT; it++) {
         if (key[r][it] != EMPTY) {
@@ -440,7 +442,7 @@ __device__ __forceinline__ void units_pass2(const CountArgs& a, Units<NT, UCAP>&
       }
 #pragma unroll
       for (int o = 1; o < G; o <<= 1) s += __shfl_xor_sync(FULL, s, o);
-      if (x < nunits && gl == 0 && s) seg_add(u.slo, u.shi, u.slot[x], s);
+      if (x < nunits && gl == 0 && s) seg_add(u.slo, u.shi, u.slot[x], (uint64_t)s);
     }
   }
 }
@@ -468,7 +470,8 @@ __device__ __forceinline__ void list_finalize(const CountArgs& a, const Store& c
     BF_CHECK(key < a.n);
     const uint32_t d = cs.get(key, kk);
     if (MODE == MODE_TOTAL) cs.zero(key, kk);
-    const uint64_t c2 = choose2(d);
+    // small tiers: d <= 128, so C(d,2) in 32 bits
+    const uint64_t c2 = SPILL ? choose2(d) : (uint64_t)((d * (d - (d > 0))) >> 1);
     lsum += c2;
     if (MODE == MODE_VERTEX && c2 && !(a.exp & 1)) red_add_u64(endpoint_slot(a, key), c2);
 #ifdef BF_PROFILE
@@ -523,7 +526,10 @@ __device__ __forceinline__ void start_passes(const CountArgs& a, Units<NT, UCAP>
     cta_sync<NT>();  // d is final
     pf.mark(3);
     if (single) {
-      units_pass2<MODE, CACHE, NT, P, G, UR, UCAP>(a, u, cs, st.kbase, cache);
+      if (st.j1 - st.j0 < (1u << 26))
+        units_pass2<MODE, CACHE, NT, P, G, UR, UCAP>(a, u, cs, st.kbase, cache);
+      else
+        units_pass2<MODE, CACHE, NT, P, G, UR, UCAP, Store, false>(a, u, cs, st.kbase, cache);
       pf.mark(5);
       cta_sync<NT>();
       pf.mark(3);
@@ -534,7 +540,10 @@ __device__ __forceinline__ void start_passes(const CountArgs& a, Units<NT, UCAP>
       while (K0 < w) {
         const uint64_t Kn = units_build<MODE, NT, P, UCAP>(a, u, jc, st.j1, base, K0, cap, par, mine, myj, myy);
         const uint32_t jn = u.jn[par];
-        units_pass2<MODE, false, NT, P, G, UR, UCAP>(a, u, cs, st.kbase, nullptr);
+        if (st.j1 - st.j0 < (1u << 26))
+          units_pass2<MODE, false, NT, P, G, UR, UCAP>(a, u, cs, st.kbase, nullptr);
+        else
+          units_pass2<MODE, false, NT, P, G, UR, UCAP, Store, false>(a, u, cs, st.kbase, nullptr);
         cta_sync<NT>();
         if (tid == 0) u.jn[par] = FULL;
         slot_flush<MODE>(a, u.slo, u.shi, mine, myj, myy);
@@ -875,7 +884,13 @@ __global__ void __launch_bounds__(SP_NT, 1) k_split_walk(CountArgs a, SplitArgs 
       const uint64_t K1 = units_build<PASS2 ? MODE : MODE_TOTAL, SP_NT, SP_P, SplitSmem::UCAP>(
           a, ss.u, jc, pc.z, base, K0, cap, par, mine, myj, myy);
       const uint32_t jn = ss.u.jn[par];
-      if (PASS2) units_pass2<MODE, false, SP_NT, SP_P, SP_G, 1, SplitSmem::UCAP>(a, ss.u, s2, kbase, nullptr);
+      if (PASS2) {
+        if (sp.z - sp.y < (1u << 26))
+          units_pass2<MODE, false, SP_NT, SP_P, SP_G, 1, SplitSmem::UCAP>(a, ss.u, s2, kbase, nullptr);
+        else
+          units_pass2<MODE, false, SP_NT, SP_P, SP_G, 1, SplitSmem::UCAP, SplitStore2, false>(a, ss.u, s2, kbase,
+                                                                                             nullptr);
+      }
       else units_pass1<false, false, SP_NT, SP_P, SP_G, 1, SplitSmem::UCAP>(a, ss.u, s1, kbase, ss.list, SP_WIN, nullptr, hashed,
                                                               nullptr);
       __syncthreads();
