@@ -258,11 +258,11 @@ struct HeavyStore {
 // d-1 stay in registers until one shared atomic per unit.
 template <int NT, uint32_t UCAP>
 struct Units {
+  static_assert(NT <= 256, "unit meta packs the slot in 8 bits");
   using SlotT = typename std::conditional<(NT <= 256), uint8_t, uint16_t>::type;
   uint32_t lo[UCAP];           // first nbr index of the unit
-  uint16_t pos[UCAP];          // chunk position of the unit's first wedge (key cache index)
-  uint8_t len[UCAP];           // 1..P
-  SlotT slot[UCAP];            // chunk-local slot (thread) of the unit
+  uint32_t meta[UCAP];         // chunk position of the first wedge (key cache index, bits 0-15)
+                               // | length 1..P (bits 16-23) | chunk-local slot (bits 24-31)
   uint32_t slo[NT], shi[NT];   // pass-2 per-slot sums (u64 as two u32)
   uint32_t wt[32];             // scan scratch
   uint32_t jn[2];              // continuation slot of chunk i in jn[i & 1] (FULL = none)
@@ -301,9 +301,7 @@ __device__ __forceinline__ void units_write(Units<NT, UCAP>& u, uint32_t lo, uin
   BF_CHECK(ex + nu <= UCAP && L < 65536);
   for (uint32_t f = 0, o = 0; f < nu; f++, o += P) {
     u.lo[ex + f] = lo + o;
-    u.pos[ex + f] = (uint16_t)(wp + o);
-    u.len[ex + f] = (uint8_t)(f + 1 < nu ? (uint32_t)P : L - o);
-    u.slot[ex + f] = (typename Units<NT, UCAP>::SlotT)threadIdx.x;
+    u.meta[ex + f] = ((wp + o) & 0xffffu) | ((f + 1 < nu ? (uint32_t)P : L - o) << 16) | (threadIdx.x << 24);
   }
   if (threadIdx.x == 0) u.nunits = total & 0xffffu;
   u.slo[threadIdx.x] = 0;
@@ -378,8 +376,9 @@ __device__ __forceinline__ void units_pass1(const CountArgs& a, Units<NT, UCAP>&
 #pragma unroll
     for (int r = 0; r < UR; r++) {
       const uint32_t x = x0 + r * NG;
-      const uint32_t lo = x < nunits ? u.lo[x] : 0u, len = x < nunits ? u.len[x] : 0u;
-      ps[r] = x < nunits ? u.pos[x] : 0u;
+      const uint32_t lo = x < nunits ? u.lo[x] : 0u, me = x < nunits ? u.meta[x] : 0u;
+      const uint32_t len = (me >> 16) & 0xffu;
+      ps[r] = me & 0xffffu;
 #pragma unroll
       for (int it = 0; it < IT; it++) {
         const uint32_t i = gl + it * G;
@@ -415,17 +414,19 @@ __device__ __forceinline__ void units_pass2(const CountArgs& a, Units<NT, UCAP>&
   const uint32_t nunits = u.nunits;
   // warp-uniform trip count: the group reduction below is a full-warp shuffle
   for (uint32_t xb = (tid & ~31u) / G; xb < nunits; xb += NG * UR) {
-    uint32_t key[UR][IT], lo[UR];
+    uint32_t key[UR][IT], lo[UR], ps[UR], sl[UR];
 #pragma unroll
     for (int r = 0; r < UR; r++) {
       const uint32_t x = xb + r * NG + (tid & 31) / G;
       const bool act = x < nunits;
       lo[r] = act ? u.lo[x] : 0u;
-      const uint32_t len = act ? u.len[x] : 0u, ps = act ? u.pos[x] : 0u;
+      const uint32_t me = act ? u.meta[x] : 0u, len = (me >> 16) & 0xffu;
+      ps[r] = me & 0xffffu;
+      sl[r] = me >> 24;
 #pragma unroll
       for (int it = 0; it < IT; it++) {
         const uint32_t i = gl + it * G;
-        key[r][it] = i < len ? (CACHE ? cache[ps + i] : __ldg(a.nbr + (lo[r] + i))) : EMPTY;
+        key[r][it] = i < len ? (CACHE ? cache[ps[r] + i] : __ldg(a.nbr + (lo[r] + i))) : EMPTY;
       }
     }
 #pragma unroll
@@ -442,7 +443,7 @@ __device__ __forceinline__ void units_pass2(const CountArgs& a, Units<NT, UCAP>&
       }
 #pragma unroll
       for (int o = 1; o < G; o <<= 1) s += __shfl_xor_sync(FULL, s, o);
-      if (x < nunits && gl == 0 && s) seg_add(u.slo, u.shi, u.slot[x], (uint64_t)s);
+      if (x < nunits && gl == 0 && s) seg_add(u.slo, u.shi, sl[r], (uint64_t)s);
     }
   }
 }
