@@ -294,3 +294,27 @@ def test_duplicate_in_large_graph(bf):
         with pytest.raises(bf.BFError) as ei:
             bf.ButterflyGraph(g.n_u, g.n_v, e)
         assert ei.value.status == bf.BF_EDUP
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_random_graphs_random_paths(bf, seed):
+    """Randomised T3: random power-law graphs, random ranking, orientation and
+    path-forcing flags (tiers, tiny windows/chunks, no split, virtual ranks);
+    every mode bit-exact with the oracle."""
+    rng = np.random.default_rng(7000 + seed)
+    n_u, n_v = int(rng.integers(50, 2500)), int(rng.integers(50, 2500))
+    m = int(min(n_u * n_v // 3, rng.integers(200, 25000)))
+    g = bfgen.chung_lu(n_u, n_v, m, float(rng.uniform(1.8, 2.6)), float(rng.uniform(1.8, 2.6)), seed=seed + 1)
+    ref = oracle.count(g.n_u, g.n_v, g.edges)
+    names = ["FORCE_WARP", "FORCE_CTA", "FORCE_DENSE", "SMALL_WINDOW", "SMALL_CHUNK", "NO_SPLIT"]
+    f = 0
+    for nm in names:
+        if rng.random() < 0.3:
+            f |= getattr(bf, "BF_FLAG_" + nm)
+    rank = ["side", "approx_degree", "degree", "auto"][int(rng.integers(0, 4))]
+    orient = ORIENTS[int(rng.integers(0, 2))]
+    opts = dict(test_flags=f)
+    if rng.random() < 0.3:
+        opts["virtual_world"] = int(rng.integers(2, 6))
+    got = run_all(bf, g, rank, orient, **opts)
+    assert_same(got, ref, f"seed {seed} flags {f:#x} {rank}/{orient} {opts}")
