@@ -75,7 +75,7 @@ struct CountArgs {
   uint32_t t0, t1;        // this tier's segment of the item list
   uint64_t S, n;          // slots, vertices (bounds checks of the debug build)
   uint32_t dbg_stop;      // debug build: stop each start after this phase (0 = never)
-  uint32_t exp;           // timing experiments (env BF_EXPERIMENT; results are wrong when set):
+  uint32_t exp;           // libbf_prof.so only: timing experiments (env BF_EXPERIMENT; results are wrong when set):
                           // 1 = skip endpoint REDs, 2 = skip centre REDs
   uint32_t win;           // dense window keys in use (<= compile-time size)
   uint32_t cap;           // heavy chunk capacity in wedges (<= HV_CAP)
@@ -1004,7 +1004,7 @@ __global__ void __launch_bounds__(256) k_split_clear(CountArgs a, SplitArgs sa) 
 #define WARP_CFG 32, BF_WARP_WIN, 512, BF_WARP_MAX_WEDGES, BF_WARP_P, BF_WARP_G, 2
 using WarpSM = SmallSmem<WARP_CFG>;
 // medium tier: 128 threads, w <= 2048, <= 128 slots
-#define MED_CFG 128, BF_MED_WIN, 2048, BF_MEDIUM_MAX_WEDGES, BF_MED_P, BF_MED_G, 2
+#define MED_CFG BF_MEDIUM_MAX_SLOTS, BF_MED_WIN, 2048, BF_MEDIUM_MAX_WEDGES, BF_MED_P, BF_MED_G, 2
 using MedSM = SmallSmem<MED_CFG>;
 // heavy tier: 256 threads, chunks of <= 8192 wedges
 #ifndef BF_BIG_NT
@@ -1025,7 +1025,7 @@ using MedSM = SmallSmem<MED_CFG>;
 #define BIG_CFG BF_BIG_NT, BF_BIG_WIN, BF_BIG_CAP, BF_BIG_LCAP, BF_BIG_P, BF_BIG_G, BF_BIG_UR
 constexpr uint64_t HV_WIN_KEYS = BF_BIG_WIN;  // BIG_CFG's window
 using BigSM = HeavySmemT<BIG_CFG>;
-static_assert(BF_WARP_MAX_SLOTS == 32 && BF_MEDIUM_MAX_SLOTS == 128, "tier slot bounds = CTA sizes");
+static_assert(BF_WARP_MAX_SLOTS == 32, "warp tier: one slot per lane");
 
 // ============================================================ output kernels
 // bv[side base + k] += sum over stripes of hub[stripe][side][k]
@@ -1158,9 +1158,9 @@ void launch_tiers(bf_graph* g, CountArgs a, const uint32_t tier[4], uint32_t* qu
   }
   if (tier[2] > tier[1]) {  // medium
     auto k = k_small<ORIENT, MODE, MED_CFG>;
-    const int grid = sms * occupancy(k, 128, sizeof(MedSM));
+    const int grid = sms * occupancy(k, BF_MEDIUM_MAX_SLOTS, sizeof(MedSM));
     a.t0 = tier[1]; a.t1 = tier[2]; a.queue = queues + 1;
-    k<<<grid, 128, sizeof(MedSM), s>>>(a);
+    k<<<grid, BF_MEDIUM_MAX_SLOTS, sizeof(MedSM), s>>>(a);
     KERNEL_CHECK(g);
   }
   if (tier[3] > tier[2]) {  // warp
@@ -1224,7 +1224,11 @@ bf_status graph_count(bf_graph* g, int mode, uint64_t* out_a, uint64_t* out_b, u
   a.olist_len = olen;
   a.S = S;
   a.n = n;
+#ifdef BF_PROFILE  // timing experiments exist only in the profile build (they break results)
   a.exp = getenv("BF_EXPERIMENT") ? (uint32_t)atoi(getenv("BF_EXPERIMENT")) : 0u;
+#else
+  a.exp = 0u;
+#endif
   a.dbg_stop = getenv("BF_DBG_STOP") ? (uint32_t)atoi(getenv("BF_DBG_STOP")) : 0u;
   a.n_u = g->n_u;
   a.n_v = g->n_v;

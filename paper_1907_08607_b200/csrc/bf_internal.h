@@ -19,7 +19,9 @@
 #ifndef BF_MEDIUM_MAX_WEDGES
 #define BF_MEDIUM_MAX_WEDGES 2048u
 #endif
-#define BF_MEDIUM_MAX_SLOTS 128u
+#ifndef BF_MEDIUM_MAX_SLOTS
+#define BF_MEDIUM_MAX_SLOTS 128u  // = the medium kernel's CTA size (one slot per thread)
+#endif
 // split starts: at most this many (largest first); row memory per batch
 constexpr uint32_t kMaxSplit = 4096;
 constexpr size_t kSplitRowBudget = (size_t)4 << 30;
