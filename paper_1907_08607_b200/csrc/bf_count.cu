@@ -473,7 +473,7 @@ __device__ __forceinline__ void list_finalize(const CountArgs& a, const Store& c
     const uint32_t key = list_get<SPILL>(list, lcap, olist, i), kk = key - kbase;
     BF_CHECK(key < a.n);
     const uint32_t d = cs.get(key, kk);
-    if (MODE == MODE_TOTAL) cs.zero(key, kk);
+    if (MODE == MODE_TOTAL && !SPILL) cs.zero(key, kk);  // heavy tier: reset after a barrier
     // small tiers: d <= 128, so C(d,2) in 32 bits
     const uint64_t c2 = SPILL ? choose2(d) : (uint64_t)((d * (d - (d > 0))) >> 1);
     lsum += c2;
@@ -526,6 +526,13 @@ __device__ __forceinline__ void start_passes(const CountArgs& a, Units<NT, UCAP>
   list_finalize<MODE, SPILL, NT>(a, cs, st.kbase, cnt, list, lcap, olist, lsum);
   if (tid == 0) pairs += cnt;
   pf.mark(4);
+  if (MODE == MODE_TOTAL && SPILL) {
+    cta_sync<NT>();
+    for (uint32_t i = tid; i < cnt; i += NT) {
+      const uint32_t key = list_get<SPILL>(list, lcap, olist, i);
+      cs.zero(key, key - st.kbase);
+    }
+  }
   if (MODE != MODE_TOTAL) {
     cta_sync<NT>();  // d is final
     pf.mark(3);
@@ -763,14 +770,14 @@ __global__ void __launch_bounds__(NT, 1) k_big(CountArgs a) {
       const uint32_t cnt = hs.u.lcnt;
       list_finalize<MODE, true, NT>(a, cs, st.kbase, cnt, hs.list, LCAP, olist, lsum);
       if (tid == 0) pair_acc += cnt;
+      __syncthreads();
       if (MODE != MODE_TOTAL) {
-        __syncthreads();
         slots_pass2<MODE, NT>(a, cs, st.j0, st.j1, st.kbase);
         __syncthreads();
-        for (uint32_t i = tid; i < cnt; i += NT) {
-          const uint32_t key = list_get<true>(hs.list, LCAP, olist, i);
-          cs.zero(key, key - st.kbase);
-        }
+      }
+      for (uint32_t i = tid; i < cnt; i += NT) {
+        const uint32_t key = list_get<true>(hs.list, LCAP, olist, i);
+        cs.zero(key, key - st.kbase);
       }
       __syncthreads();
       if (tid == 0) hs.u.lcnt = 0;
