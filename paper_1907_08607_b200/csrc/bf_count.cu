@@ -482,7 +482,7 @@ __device__ __forceinline__ void list_finalize(const CountArgs& a, const Store& c
     lsum += c2;
     if (MODE == MODE_VERTEX && c2 && !(a.exp & 1)) red_add_u64(endpoint_slot(a, key), c2);
 #ifdef BF_PROFILE
-    if (c2) {
+    if (c2 && (a.exp & 64)) {
       const uint32_t kk2 = key - (key >= a.n_u ? a.n_u : 0u);
       atomicAdd(&g_prof_red[0], 1ull);
       if (kk2 < 256) atomicAdd(&g_prof_red[1], 1ull);
