@@ -986,14 +986,17 @@ __global__ void __launch_bounds__(256) k_split_clear(CountArgs a, SplitArgs sa) 
 
 // tier configurations <NT, WIN, HS|CAP, CAP|LCAP, P, G, UR>
 // warp tier: 1-warp CTAs, w <= 512, <= 32 slots
+// window sizes: smaller windows trade overflow-path work for occupancy;
+// measured on c2 / c3 (warp, big): (4096, 8192) 7.73 / 92.6 ms,
+// (2048, 4096) 7.06, (1024, 4096) 6.97 / 85.6 ms, (512, 4096) 7.10
 #ifndef BF_WARP_WIN
-#define BF_WARP_WIN 4096
+#define BF_WARP_WIN 1024
 #endif
 #ifndef BF_MED_WIN
 #define BF_MED_WIN 8192
 #endif
 #ifndef BF_BIG_WIN
-#define BF_BIG_WIN 8192
+#define BF_BIG_WIN 4096
 #endif
 // unit shape: P wedges per unit, G lanes per unit.  G = 8 makes every lane
 // group read one 32-byte sector per step; the wedge walks are bound by L1/
@@ -1014,10 +1017,16 @@ __global__ void __launch_bounds__(256) k_split_clear(CountArgs a, SplitArgs sa) 
 #ifndef BF_BIG_G
 #define BF_BIG_G 8
 #endif
-#define WARP_CFG 32, BF_WARP_WIN, 512, BF_WARP_MAX_WEDGES, BF_WARP_P, BF_WARP_G, 2
+#ifndef BF_WARP_UR
+#define BF_WARP_UR 2
+#endif
+#ifndef BF_MED_UR
+#define BF_MED_UR 2
+#endif
+#define WARP_CFG 32, BF_WARP_WIN, 512, BF_WARP_MAX_WEDGES, BF_WARP_P, BF_WARP_G, BF_WARP_UR
 using WarpSM = SmallSmem<WARP_CFG>;
 // medium tier: 128 threads, w <= 2048, <= 128 slots
-#define MED_CFG BF_MEDIUM_MAX_SLOTS, BF_MED_WIN, 2048, BF_MEDIUM_MAX_WEDGES, BF_MED_P, BF_MED_G, 2
+#define MED_CFG BF_MEDIUM_MAX_SLOTS, BF_MED_WIN, 2048, BF_MEDIUM_MAX_WEDGES, BF_MED_P, BF_MED_G, BF_MED_UR
 using MedSM = SmallSmem<MED_CFG>;
 // heavy tier: 256 threads, chunks of <= 8192 wedges
 #ifndef BF_BIG_NT
