@@ -737,8 +737,11 @@ struct HeavySmemT {
   uint32_t list[LCAP];
 };
 
+#ifndef BF_BIG_MINB
+#define BF_BIG_MINB 1
+#endif
 template <int ORIENT, int MODE, int NT, uint32_t WIN, uint32_t CAP, uint32_t LCAP, int P, int G, int UR>
-__global__ void __launch_bounds__(NT, 1) k_big(CountArgs a) {
+__global__ void __launch_bounds__(NT, BF_BIG_MINB) k_big(CountArgs a) {
   using SM = HeavySmemT<NT, WIN, CAP, LCAP, P, G, UR>;
   extern __shared__ __align__(16) char sm[];
   SM& hs = *(SM*)sm;
@@ -1090,6 +1093,9 @@ inline unsigned grid_for(size_t n, int sms) {
 template <class K>
 int occupancy(K kernel, int threads, size_t smem) {
   CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+#ifdef BF_CARVEOUT  // tuning: shared-memory carve-out in percent (the rest is L1)
+  CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, BF_CARVEOUT));
+#endif
   int b = 0;
   CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, threads, smem));
   return b > 0 ? b : 1;
