@@ -1202,7 +1202,10 @@ void launch_tiers(bf_graph* g, CountArgs a, const uint32_t tier[4], uint32_t* qu
   }
   if (tier[3] > tier[2]) {  // warp
     auto k = k_small<ORIENT, MODE, WARP_CFG>;
-    const int grid = sms * occupancy(k, 32, sizeof(WarpSM));
+#ifndef BF_WARP_BLOCKS
+#define BF_WARP_BLOCKS 64
+#endif
+    const int grid = sms * std::min(occupancy(k, 32, sizeof(WarpSM)), BF_WARP_BLOCKS);
     a.t0 = tier[2]; a.t1 = tier[3]; a.queue = queues + 2;
     k<<<grid, 32, sizeof(WarpSM), s>>>(a);
     KERNEL_CHECK(g);
