@@ -111,23 +111,34 @@ constexpr int RS_ITEMS = 8;                        // rounds per warp
 constexpr int RS_TILE = RS_THREADS * RS_ITEMS;     // 2048 keys per tile
 constexpr int RS_WARP_SPAN = 32 * RS_ITEMS;        // keys per warp (contiguous)
 
+// tile digit histogram: all loads first (RS_ITEMS in flight per thread), then
+// per-warp shared histograms with plain atomics (digits of sorted-ish keys
+// repeat, but a per-warp copy keeps same-address contention within a warp),
+// summed per digit at the end
 template <class K>
 __global__ void __launch_bounds__(RS_THREADS) k_rs_upsweep(const K* __restrict__ keys, size_t n, int shift,
                                                            uint32_t* __restrict__ counts, uint32_t ntiles) {
-  __shared__ uint32_t h[256];
-  h[threadIdx.x] = 0;
+  __shared__ uint32_t h[RS_WARPS][256];
+  for (int i = threadIdx.x; i < RS_WARPS * 256; i += RS_THREADS) (&h[0][0])[i] = 0;
   __syncthreads();
-  size_t base = (size_t)blockIdx.x * RS_TILE;
-  int lane = threadIdx.x & 31;
+  const size_t base = (size_t)blockIdx.x * RS_TILE;
+  const int w = threadIdx.x >> 5;
+  K k[RS_ITEMS];
 #pragma unroll
   for (int i = 0; i < RS_ITEMS; i++) {
-    size_t idx = base + (size_t)i * RS_THREADS + threadIdx.x;
-    uint32_t d = idx < n ? (uint32_t)((keys[idx] >> shift) & 255) : 256u;
-    unsigned peers = __match_any_sync(0xffffffffu, d);
-    if (d < 256 && (peers >> lane) == 1u) atomicAdd(&h[d], (uint32_t)__popc(peers));
+    const size_t idx = base + (size_t)i * RS_THREADS + threadIdx.x;
+    k[i] = idx < n ? keys[idx] : (K)0;
+  }
+#pragma unroll
+  for (int i = 0; i < RS_ITEMS; i++) {
+    const size_t idx = base + (size_t)i * RS_THREADS + threadIdx.x;
+    if (idx < n) atomicAdd(&h[w][(uint32_t)((k[i] >> shift) & 255)], 1u);
   }
   __syncthreads();
-  counts[(size_t)threadIdx.x * ntiles + blockIdx.x] = h[threadIdx.x];
+  uint32_t c = 0;
+#pragma unroll
+  for (int ww = 0; ww < RS_WARPS; ww++) c += h[ww][threadIdx.x];
+  counts[(size_t)threadIdx.x * ntiles + blockIdx.x] = c;
 }
 
 template <class K, bool VALS>
