@@ -161,11 +161,16 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_downsweep(const K* __restrict
   uint32_t val[RS_ITEMS];
   uint32_t rk[RS_ITEMS];
 #pragma unroll
-  for (int r = 0; r < RS_ITEMS; r++) {
+  for (int r = 0; r < RS_ITEMS; r++) {  // all loads in flight before the ranking
     size_t idx = tbase + (size_t)w * RS_WARP_SPAN + r * 32 + lane;
     bool valid = idx < n;
     key[r] = valid ? kin[idx] : (K)0;
     if (VALS) val[r] = valid ? vin[idx] : 0u;
+  }
+#pragma unroll
+  for (int r = 0; r < RS_ITEMS; r++) {
+    size_t idx = tbase + (size_t)w * RS_WARP_SPAN + r * 32 + lane;
+    bool valid = idx < n;
     uint32_t d = valid ? (uint32_t)((key[r] >> shift) & 255) : 256u;
     unsigned peers = __match_any_sync(0xffffffffu, d);
     uint32_t before = valid ? wcnt[w][d] : 0u;
