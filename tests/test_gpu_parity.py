@@ -318,3 +318,13 @@ def test_random_graphs_random_paths(bf, seed):
         opts["virtual_world"] = int(rng.integers(2, 6))
     got = run_all(bf, g, rank, orient, **opts)
     assert_same(got, ref, f"seed {seed} flags {f:#x} {rank}/{orient} {opts}")
+
+
+def test_nccl_bootstrap_single_rank(bf):
+    """The multi-GPU bootstrap on one GPU: NCCL loads at run time, a 1-rank
+    communicator is created from the 128-byte id and destroyed."""
+    uid = bf.bf_nccl_unique_id()
+    assert isinstance(uid, bytes) and len(uid) == 128
+    comm = bf.bf_nccl_comm_create(uid, 0, 1, 0)
+    assert comm
+    bf.bf_nccl_comm_destroy(comm)
