@@ -90,6 +90,9 @@ typedef enum { BF_ORIENT_AUTO = 0, BF_ORIENT_LOW = 1, BF_ORIENT_HIGH = 2 } bf_or
                                          more wedges takes the multi-chunk path; the
                                          split threshold drops to 256 wedges            */
 #define BF_FLAG_NO_SPLIT        0x40u /* never split a start across CTAs                */
+#define BF_FLAG_UNPACKED_SORT   0x80u /* bf_rank: slot sort with separate key and value
+                                         arrays (the path taken when rank bits + edge-id
+                                         bits exceed 64)                                */
 
 typedef struct {
   int device;               /* CUDA ordinal                                           */

@@ -31,7 +31,7 @@ RANK_NAMES = {v: k for k, v in RANK_KINDS.items()}
 BF_ORIENT_AUTO, BF_ORIENT_LOW, BF_ORIENT_HIGH = 0, 1, 2
 ORIENTS = {"auto": BF_ORIENT_AUTO, "low": BF_ORIENT_LOW, "high": BF_ORIENT_HIGH}
 BF_FLAG_FORCE_WARP, BF_FLAG_FORCE_CTA, BF_FLAG_SMALL_WINDOW, BF_FLAG_FORCE_DENSE = 0x1, 0x2, 0x4, 0x10
-BF_FLAG_SMALL_CHUNK, BF_FLAG_NO_SPLIT = 0x20, 0x40
+BF_FLAG_SMALL_CHUNK, BF_FLAG_NO_SPLIT, BF_FLAG_UNPACKED_SORT = 0x20, 0x40, 0x80
 
 
 class bf_options(ctypes.Structure):

@@ -28,10 +28,10 @@ inline unsigned grid_for(size_t n, int sms) {
 // degree increments are aggregated over the lanes of a warp that hold the same
 // vertex (__match_any_sync): power-law hubs (c4's Zipf items) would otherwise
 // serialise thousands of atomics on one address
-__device__ __forceinline__ void add_degree(uint32_t* deg, uint64_t z, bool valid) {
+__device__ __forceinline__ void add_degree(uint32_t* deg, uint32_t z, bool valid) {
   const uint32_t act = __ballot_sync(0xffffffffu, valid);
   if (!valid) return;
-  const uint32_t peers = __match_any_sync(act, (unsigned long long)z);
+  const uint32_t peers = __match_any_sync(act, z);  // gid < n <= 2^32: a 32-bit match
   if ((threadIdx.x & 31) == (uint32_t)(__ffs(peers) - 1)) atomicAdd(&deg[z], (uint32_t)__popc(peers));
 }
 
@@ -49,7 +49,7 @@ __global__ void k_validate_degree(const uint32_t* __restrict__ e, uint64_t m, ui
       if (!ok) atomicOr(flags, 1u);
     }
     add_degree(deg, uv.x, ok);
-    add_degree(deg, (uint64_t)nU + uv.y, ok);
+    add_degree(deg, nU + uv.y, ok);
   }
 }
 
@@ -142,29 +142,28 @@ __global__ void k_auto_w(const uint32_t* __restrict__ deg, const uint32_t* __res
 }
 
 // ---- a3 -----------------------------------------------------------------------
-__global__ void k_slot_keys(const uint32_t* __restrict__ e, uint64_t m, uint32_t nU, uint64_t n, int B,
-                            const uint32_t* __restrict__ rid_of_gid, uint64_t* __restrict__ keys,
+// rids are side-major (U in [0, nU), V in [nU, n)), so the U-end slots fill
+// the first m CSR positions and the V-end slots the last m: two sorts of m
+// keys with side-local bits, (src asc, dst rid desc): U slot i at keys[i], V
+// slot i at keys[m + i].  With Be > 0 the edge id i sits in the low Be bits of
+// the same u64 (no value arrays); else vals hold the slot ids 2i / 2i+1.
+__global__ void k_slot_keys(const uint32_t* __restrict__ e, uint64_t m, uint32_t nU, uint64_t n, int Bu, int Bv,
+                            int Be, const uint32_t* __restrict__ rid_of_gid, uint64_t* __restrict__ keys,
                             uint32_t* __restrict__ vals) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
     uint2 uv = reinterpret_cast<const uint2*>(e)[i];
     uint64_t ru = rid_of_gid[uv.x], rv = rid_of_gid[(uint64_t)nU + uv.y];
-    keys[2 * i] = (ru << B) | (n - 1 - rv);  // src U: (rid asc, dst rid desc)
-    keys[2 * i + 1] = (rv << B) | (n - 1 - ru);
-    vals[2 * i] = (uint32_t)(2 * i);
-    vals[2 * i + 1] = (uint32_t)(2 * i + 1);
-  }
-}
-
-__global__ void k_slot_decode(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ vals, uint64_t S,
-                              uint64_t n, int B, uint32_t* __restrict__ nbr, uint32_t* __restrict__ src,
-                              uint32_t* __restrict__ where) {
-  uint64_t mask = (B >= 64) ? ~0ull : ((1ull << B) - 1);
-  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < S; j += (uint64_t)gridDim.x * blockDim.x) {
-    uint64_t k = keys[j];
-    uint32_t v = vals[j];
-    nbr[j] = (uint32_t)(n - 1 - (k & mask));
-    src[j] = (uint32_t)(k >> B);
-    where[v] = (uint32_t)j;  // where[2e] / where[2e+1] = slot of edge e from its U / V end
+    const uint64_t ku = (ru << Bv) | (n - 1 - rv);                    // nbr_last = n-1
+    const uint64_t kv = ((rv - nU) << Bu) | ((uint64_t)nU - 1 - ru);  // nbr_last = nU-1, src_base = nU
+    if (Be) {
+      keys[i] = (ku << Be) | i;
+      keys[m + i] = (kv << Be) | i;
+    } else {
+      keys[i] = ku;
+      keys[m + i] = kv;
+      vals[i] = (uint32_t)(2 * i);
+      vals[m + i] = (uint32_t)(2 * i + 1);
+    }
   }
 }
 
@@ -434,7 +433,9 @@ bf_status graph_rank(bf_graph* g, int kind) {
   scan_exclusive_u32(deg_rid, g->off.as<uint32_t>(), n, g->off.as<uint32_t>() + n, tmp, s, L);
 
   // ---- a3: slots sorted by (rid(src) asc, rid(dst) desc) --------------------
-  int B = std::max(1, ceil_log2_u64(n1));
+  // side-local key widths: U slots (ru, n-1-rv), V slots (rv-nU, nU-1-ru)
+  const int Bu = std::max(1, ceil_log2_u64(std::max<uint64_t>(g->n_u, 1)));
+  const int Bv = std::max(1, ceil_log2_u64(std::max<uint64_t>(g->n_v, 1)));
   uint64_t* k0 = g->tmp_a.as<uint64_t>();
   uint64_t* k1 = g->tmp_b.as<uint64_t>();
   uint32_t* v0 = g->tmp_c.as<uint32_t>();
@@ -443,16 +444,20 @@ bf_status graph_rank(bf_graph* g, int kind) {
   g->dflag.ensure(16);
   CUDA_TRY(cudaMemsetAsync(g->dflag.p, 0, 4, s));
   if (m) {
-    k_slot_keys<<<grid_for(m, g->sms), TPB, 0, s>>>(g->edges.as<uint32_t>(), m, g->n_u, n, B,
+    const int Be0 = std::max(1, ceil_log2_u64(m));
+    const int Be = (Bu + Bv + Be0 <= 64 && !(g->opt.test_flags & BF_FLAG_UNPACKED_SORT)) ? Be0 : 0;  // pack when it fits
+    k_slot_keys<<<grid_for(m, g->sms), TPB, 0, s>>>(g->edges.as<uint32_t>(), m, g->n_u, n, Bu, Bv, Be,
                                                      g->rid_of_gid.as<uint32_t>(), k0, v0);
     KERNEL_CHECK(g);
-    int w2 = radix_sort_u64(k0, v0, k1, v1, S, 0, 2 * B, tmp, s, L);
-    uint64_t* ks = w2 ? k1 : k0;
-    uint32_t* vs = w2 ? v1 : v0;
     uint32_t* src = g->tmp_f.as<uint32_t>();
     uint32_t* where = g->where.as<uint32_t>();
-    k_slot_decode<<<grid_for(S, g->sms), TPB, 0, s>>>(ks, vs, S, n, B, g->nbr.as<uint32_t>(), src, where);
-    KERNEL_CHECK(g);
+    uint32_t* nbr = g->nbr.as<uint32_t>();
+    // U half: nbr = (n-1) - low, src = high; V half: nbr = (nU-1) - low, src = nU + high
+    const int wu = radix_sort_slots(k0, v0, k1, v1, m, Bu + Bv, Bv, Be, 0, n - 1, 0, 0, nbr, src, where, tmp, s, L);
+    const int wv = radix_sort_slots(k0 + m, v0 + m, k1 + m, v1 + m, m, Bu + Bv, Bu, Be, 1, (uint64_t)g->n_u - 1,
+                                    g->n_u, m, nbr + m, src + m, where, tmp, s, L);
+    if (wu != wv) CUDA_TRY(cudaMemcpyAsync(wu ? v0 : v1, wu ? v1 : v0, m * 4, cudaMemcpyDeviceToDevice, s));
+    uint32_t* vs = wv ? v1 : v0;  // slot ids in CSR order
     k_pos_hi<<<grid_for(S, g->sms), TPB, 0, s>>>(vs, where, g->nbr.as<uint32_t>(), src, g->off.as<uint32_t>(),
                                                   g->rkey.as<uint64_t>(), S, g->pos.as<uint32_t>(),
                                                   g->hi.as<uint32_t>(), g->dflag.as<uint32_t>());

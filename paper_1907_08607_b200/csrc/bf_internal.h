@@ -69,6 +69,15 @@ int radix_sort_u32(uint32_t* k0, uint32_t* v0, uint32_t* k1, uint32_t* v1, size_
                    int end_bit, void* temp, cudaStream_t s, uint64_t* launches);
 int radix_sort_u64(uint64_t* k0, uint32_t* v0, uint64_t* k1, uint32_t* v1, size_t n, int begin_bit,
                    int end_bit, void* temp, cudaStream_t s, uint64_t* launches);
+// a slot sort whose last pass writes the decoded CSR range directly: keys are
+// (src - src_base) << B | (nbr_last - nbr) (key_bits wide), either with u32
+// values = slot ids (Be = 0) or packed above a Be-bit edge id (slot id =
+// 2e + side, no values); writes nbr / src / where[slot id] = pos_base + p
+// (pointers already offset to the range) and the slot ids in CSR order to v0
+// (return 0) or v1 (return 1)
+int radix_sort_slots(uint64_t* k0, uint32_t* v0, uint64_t* k1, uint32_t* v1, size_t n, int key_bits, int B, int Be,
+                     int side, uint64_t nbr_last, uint64_t src_base, uint64_t pos_base, uint32_t* nbr, uint32_t* src,
+                     uint32_t* where, void* temp, cudaStream_t s, uint64_t* launches);
 
 static inline int ceil_log2_u64(uint64_t x) {  // bits needed to hold values < x (x>=1)
   int b = 0;

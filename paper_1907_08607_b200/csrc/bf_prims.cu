@@ -1,6 +1,6 @@
 // bf_prims.cu -- hand-written device primitives for the CSR builder (layer B0):
 // exclusive prefix scan (reduce-then-scan, recursive over tile sums) and a
-// stable LSD radix sort (8-bit digits: tile histogram -> digit-major scan ->
+// stable LSD radix sort (<= 8-bit digits: tile histogram -> digit-major scan ->
 // stable scatter through shared memory).  Paper: "prefix sum" P:256-262 and
 // "parallel integer sort" P:668-677 (§2, §4.1).
 #include "bf_internal.h"
@@ -107,22 +107,28 @@ void scan_impl(const TI* in, TO* out, size_t n, TO* total, TO* temp, cudaStream_
 // ---------------------------------------------------------------- radix sort
 constexpr int RS_THREADS = 256;
 constexpr int RS_WARPS = RS_THREADS / 32;
-constexpr int RS_ITEMS = 8;                        // rounds per warp
+#ifndef BF_RS_ITEMS
+#define BF_RS_ITEMS 8
+#endif
+constexpr int RS_ITEMS = BF_RS_ITEMS;              // rounds per warp
 constexpr int RS_TILE = RS_THREADS * RS_ITEMS;     // 2048 keys per tile
 constexpr int RS_WARP_SPAN = 32 * RS_ITEMS;        // keys per warp (contiguous)
 
 // tile digit histogram: all loads first (RS_ITEMS in flight per thread), then
 // per-warp shared histograms with plain atomics (digits of sorted-ish keys
 // repeat, but a per-warp copy keeps same-address contention within a warp),
-// summed per digit at the end
+// summed per digit at the end.  Digits are `bits` <= 8 wide (the passes of one
+// sort share the key's width evenly: a 42-bit key sorts in 6 passes of 7 bits,
+// whose longer per-digit runs coalesce the scatter better than 8-bit digits).
 template <class K>
-__global__ void __launch_bounds__(RS_THREADS) k_rs_upsweep(const K* __restrict__ keys, size_t n, int shift,
+__global__ void __launch_bounds__(RS_THREADS) k_rs_upsweep(const K* __restrict__ keys, size_t n, int shift, int bits,
                                                            uint32_t* __restrict__ counts, uint32_t ntiles) {
   __shared__ uint32_t h[RS_WARPS][256];
   for (int i = threadIdx.x; i < RS_WARPS * 256; i += RS_THREADS) (&h[0][0])[i] = 0;
   __syncthreads();
   const size_t base = (size_t)blockIdx.x * RS_TILE;
   const int w = threadIdx.x >> 5;
+  const uint32_t mask = (1u << bits) - 1u;
   K k[RS_ITEMS];
 #pragma unroll
   for (int i = 0; i < RS_ITEMS; i++) {
@@ -132,20 +138,34 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_upsweep(const K* __restrict__
 #pragma unroll
   for (int i = 0; i < RS_ITEMS; i++) {
     const size_t idx = base + (size_t)i * RS_THREADS + threadIdx.x;
-    if (idx < n) atomicAdd(&h[w][(uint32_t)((k[i] >> shift) & 255)], 1u);
+    if (idx < n) atomicAdd(&h[w][(uint32_t)(k[i] >> shift) & mask], 1u);
   }
   __syncthreads();
-  uint32_t c = 0;
+  if (threadIdx.x <= mask) {
+    uint32_t c = 0;
 #pragma unroll
-  for (int ww = 0; ww < RS_WARPS; ww++) c += h[ww][threadIdx.x];
-  counts[(size_t)threadIdx.x * ntiles + blockIdx.x] = c;
+    for (int ww = 0; ww < RS_WARPS; ww++) c += h[ww][threadIdx.x];
+    counts[(size_t)threadIdx.x * ntiles + blockIdx.x] = c;
+  }
 }
+
+// the last pass of the slot sort may write the decoded CSR instead of keys and
+// values.  A slot's record is either (key, value) with value = slot id, or one
+// u64 key | edge id (Be low bits; the slot id is 2e + side) when both fit.
+struct RadixDecode {
+  uint32_t* nbr;    // nbr[p] = nbr_last - (key & low B bits)
+  uint32_t* src;    // src[p] = src_base + (key >> B)
+  uint32_t* where;  // where[slot id] = pos_base + p
+  uint32_t* vals;   // vals[p] = slot id
+  uint64_t nbr_last, src_base, pos_base;
+  int B, Be, side;
+};
 
 template <class K, bool VALS>
 __global__ void __launch_bounds__(RS_THREADS) k_rs_downsweep(const K* __restrict__ kin, const uint32_t* __restrict__ vin,
                                                              K* __restrict__ kout, uint32_t* __restrict__ vout, size_t n,
-                                                             int shift, const uint32_t* __restrict__ offs,
-                                                             uint32_t ntiles) {
+                                                             int shift, int bits, const uint32_t* __restrict__ offs,
+                                                             uint32_t ntiles, RadixDecode dec) {
   __shared__ K skeys[RS_TILE];
   __shared__ uint32_t svals[VALS ? RS_TILE : 1];
   __shared__ uint32_t wcnt[RS_WARPS][256];
@@ -153,8 +173,9 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_downsweep(const K* __restrict
   __shared__ uint32_t goff[256];
   __shared__ uint32_t wt[32];
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const uint32_t mask = (1u << bits) - 1u;
   for (int i = tid; i < RS_WARPS * 256; i += RS_THREADS) (&wcnt[0][0])[i] = 0;
-  goff[tid] = offs[(size_t)tid * ntiles + blockIdx.x];
+  goff[tid] = (uint32_t)tid <= mask ? offs[(size_t)tid * ntiles + blockIdx.x] : 0u;
   __syncthreads();
   const size_t tbase = (size_t)blockIdx.x * RS_TILE;
   K key[RS_ITEMS];
@@ -171,7 +192,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_downsweep(const K* __restrict
   for (int r = 0; r < RS_ITEMS; r++) {
     size_t idx = tbase + (size_t)w * RS_WARP_SPAN + r * 32 + lane;
     bool valid = idx < n;
-    uint32_t d = valid ? (uint32_t)((key[r] >> shift) & 255) : 256u;
+    uint32_t d = valid ? ((uint32_t)(key[r] >> shift) & mask) : 256u;
     unsigned peers = __match_any_sync(0xffffffffu, d);
     uint32_t before = valid ? wcnt[w][d] : 0u;
     rk[r] = before + (uint32_t)__popc(peers & ((1u << lane) - 1u));
@@ -195,7 +216,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_downsweep(const K* __restrict
   for (int r = 0; r < RS_ITEMS; r++) {
     size_t idx = tbase + (size_t)w * RS_WARP_SPAN + r * 32 + lane;
     if (idx < n) {
-      uint32_t d = (uint32_t)((key[r] >> shift) & 255);
+      uint32_t d = (uint32_t)(key[r] >> shift) & mask;
       uint32_t p = dstart[d] + wcnt[w][d] + rk[r];
       skeys[p] = key[r];
       if (VALS) svals[p] = val[r];
@@ -203,9 +224,25 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_downsweep(const K* __restrict
   }
   __syncthreads();
   uint32_t cnt = (uint32_t)min((size_t)RS_TILE, n - tbase);
+  if (dec.nbr) {  // final pass of the slot sort: decode in place of the key/value write
+    const uint64_t lmask = (dec.B >= 64) ? ~0ull : ((1ull << dec.B) - 1);
+    const uint64_t emask = (1ull << dec.Be) - 1;
+    for (uint32_t i = tid; i < cnt; i += RS_THREADS) {
+      const uint64_t kr = (uint64_t)skeys[i];
+      const uint32_t d = (uint32_t)(kr >> shift) & mask;
+      const size_t gp = (size_t)goff[d] + (i - dstart[d]);
+      const uint64_t k = kr >> dec.Be;
+      const uint32_t slot = VALS ? svals[i] : (uint32_t)(2 * (kr & emask) + dec.side);
+      dec.nbr[gp] = (uint32_t)(dec.nbr_last - (k & lmask));
+      dec.src[gp] = (uint32_t)(dec.src_base + (k >> dec.B));
+      dec.vals[gp] = slot;
+      dec.where[slot] = (uint32_t)(dec.pos_base + gp);
+    }
+    return;
+  }
   for (uint32_t i = tid; i < cnt; i += RS_THREADS) {
     K k = skeys[i];
-    uint32_t d = (uint32_t)((k >> shift) & 255);
+    uint32_t d = (uint32_t)(k >> shift) & mask;
     size_t gp = (size_t)goff[d] + (i - dstart[d]);
     kout[gp] = k;
     if (VALS) vout[gp] = svals[i];
@@ -214,22 +251,28 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_downsweep(const K* __restrict
 
 template <class K>
 int radix_impl(K* k0, uint32_t* v0, K* k1, uint32_t* v1, size_t n, int begin_bit, int end_bit, void* temp,
-               cudaStream_t s, uint64_t* launches) {
-  if (n <= 1 || end_bit <= begin_bit) return 0;
+               cudaStream_t s, uint64_t* launches, const RadixDecode* dec = nullptr) {
+  if (n == 0 || end_bit <= begin_bit) return 0;
+  const int span = end_bit - begin_bit;
+  const int passes = (span + 7) / 8;
+  const int bits = (span + passes - 1) / passes;
   uint32_t ntiles = (uint32_t)((n + RS_TILE - 1) / RS_TILE);
-  size_t ncounts = (size_t)ntiles * 256;
+  size_t ncounts = (size_t)ntiles << bits;
   uint32_t* counts = (uint32_t*)temp;
-  uint32_t* stemp = counts + ncounts + 64;
+  uint32_t* stemp = counts + (size_t)ntiles * 256 + 64;
   K* ki = k0; K* ko = k1;
   uint32_t* vi = v0; uint32_t* vo = v1;
   int which = 0;
-  for (int sh = begin_bit; sh < end_bit; sh += 8) {
-    k_rs_upsweep<K><<<ntiles, RS_THREADS, 0, s>>>(ki, n, sh, counts, ntiles);
+  const RadixDecode none = {nullptr, nullptr, nullptr, nullptr, 0, 0, 0, 0, 0, 0};
+  for (int p = 0, sh = begin_bit; p < passes; p++, sh += bits) {
+    RadixDecode d = (dec && p == passes - 1) ? *dec : none;
+    if (d.nbr && !d.vals) d.vals = vo;  // (key, value) records: slot ids to the pass's value output
+    k_rs_upsweep<K><<<ntiles, RS_THREADS, 0, s>>>(ki, n, sh, bits, counts, ntiles);
     (*launches)++;
     CUDA_TRY(cudaGetLastError());
     scan_impl<uint32_t, uint32_t>(counts, counts, ncounts, nullptr, stemp, s, launches);
-    if (vi) k_rs_downsweep<K, true><<<ntiles, RS_THREADS, 0, s>>>(ki, vi, ko, vo, n, sh, counts, ntiles);
-    else k_rs_downsweep<K, false><<<ntiles, RS_THREADS, 0, s>>>(ki, nullptr, ko, nullptr, n, sh, counts, ntiles);
+    if (vi) k_rs_downsweep<K, true><<<ntiles, RS_THREADS, 0, s>>>(ki, vi, ko, vo, n, sh, bits, counts, ntiles, d);
+    else k_rs_downsweep<K, false><<<ntiles, RS_THREADS, 0, s>>>(ki, nullptr, ko, nullptr, n, sh, bits, counts, ntiles, d);
     (*launches)++;
     CUDA_TRY(cudaGetLastError());
     K* t = ki; ki = ko; ko = t;
@@ -266,4 +309,15 @@ int radix_sort_u32(uint32_t* k0, uint32_t* v0, uint32_t* k1, uint32_t* v1, size_
 int radix_sort_u64(uint64_t* k0, uint32_t* v0, uint64_t* k1, uint32_t* v1, size_t n, int begin_bit, int end_bit,
                    void* temp, cudaStream_t s, uint64_t* launches) {
   return radix_impl<uint64_t>(k0, v0, k1, v1, n, begin_bit, end_bit, temp, s, launches);
+}
+int radix_sort_slots(uint64_t* k0, uint32_t* v0, uint64_t* k1, uint32_t* v1, size_t n, int key_bits, int B, int Be,
+                     int side, uint64_t nbr_last, uint64_t src_base, uint64_t pos_base, uint32_t* nbr, uint32_t* src,
+                     uint32_t* where, void* temp, cudaStream_t s, uint64_t* launches) {
+  RadixDecode dec = {nbr, src, where, nullptr, nbr_last, src_base, pos_base, B, Be, side};
+  if (Be) {  // packed records: slot ids to v0
+    dec.vals = v0;
+    radix_impl<uint64_t>(k0, nullptr, k1, nullptr, n, Be, Be + key_bits, temp, s, launches, &dec);
+    return 0;
+  }
+  return radix_impl<uint64_t>(k0, v0, k1, v1, n, 0, key_bits, temp, s, launches, &dec);
 }

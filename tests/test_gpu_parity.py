@@ -93,7 +93,8 @@ def test_random_small(bf, seed):
 
 @pytest.mark.parametrize("flags", ["warp", "cta", "dense", "small_window", "dense+small_window", "light8",
                                    "small_chunk", "dense+small_chunk", "dense+small_window+small_chunk",
-                                   "cta+small_window", "small_chunk+small_window", "dense+no_split+small_chunk"])
+                                   "cta+small_window", "small_chunk+small_window", "dense+no_split+small_chunk",
+                                   "unpacked_sort"])
 @pytest.mark.parametrize("orient", ORIENTS)
 def test_forced_paths(bf, flags, orient):
     """T3: every start through one tier; tiny windows force the overflow paths
@@ -113,6 +114,8 @@ def test_forced_paths(bf, flags, orient):
         f |= bf.BF_FLAG_SMALL_CHUNK  # also drops the split threshold: giant-start pieces
     if "no_split" in flags:
         f |= bf.BF_FLAG_NO_SPLIT
+    if "unpacked_sort" in flags:
+        f |= bf.BF_FLAG_UNPACKED_SORT  # the c5-size slot sort (key and value arrays)
     opts = dict(test_flags=f)
     if flags == "light8":
         opts["test_light_max_wedges"] = 8
@@ -291,9 +294,10 @@ def test_duplicate_in_large_graph(bf):
     for pick in (0, 12345, g.m - 1):
         e = np.concatenate([g.edges, g.edges[pick:pick + 1]])
         e = e[np.random.default_rng(pick).permutation(len(e))]
-        with pytest.raises(bf.BFError) as ei:
-            bf.ButterflyGraph(g.n_u, g.n_v, e)
-        assert ei.value.status == bf.BF_EDUP
+        for f in (0, bf.BF_FLAG_UNPACKED_SORT):
+            with pytest.raises(bf.BFError) as ei:
+                bf.ButterflyGraph(g.n_u, g.n_v, e, test_flags=f)
+            assert ei.value.status == bf.BF_EDUP
 
 
 @pytest.mark.parametrize("seed", range(16))
@@ -306,7 +310,7 @@ def test_random_graphs_random_paths(bf, seed):
     m = int(min(n_u * n_v // 3, rng.integers(200, 25000)))
     g = bfgen.chung_lu(n_u, n_v, m, float(rng.uniform(1.8, 2.6)), float(rng.uniform(1.8, 2.6)), seed=seed + 1)
     ref = oracle.count(g.n_u, g.n_v, g.edges)
-    names = ["FORCE_WARP", "FORCE_CTA", "FORCE_DENSE", "SMALL_WINDOW", "SMALL_CHUNK", "NO_SPLIT"]
+    names = ["FORCE_WARP", "FORCE_CTA", "FORCE_DENSE", "SMALL_WINDOW", "SMALL_CHUNK", "NO_SPLIT", "UNPACKED_SORT"]
     f = 0
     for nm in names:
         if rng.random() < 0.3:
