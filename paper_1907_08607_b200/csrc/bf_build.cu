@@ -167,22 +167,35 @@ __global__ void k_slot_keys(const uint32_t* __restrict__ e, uint64_t m, uint32_t
   }
 }
 
-// also rejects repeated edges: after the slot sort a repeated (u,v) pair is
-// two adjacent equal slots of the same source (reading Z8)
-__global__ void k_pos_hi(const uint32_t* __restrict__ vals, const uint32_t* __restrict__ where,
-                         const uint32_t* __restrict__ nbr, const uint32_t* __restrict__ src,
-                         const uint32_t* __restrict__ off, const uint64_t* __restrict__ rkey, uint64_t S,
-                         uint32_t* __restrict__ pos, uint32_t* __restrict__ hi, uint32_t* __restrict__ flags) {
+// pos[x->y] = index of x in N(y) (the twin slot's offset in y's row); also
+// rejects repeated edges: after the slot sort a repeated (u,v) pair is two
+// adjacent equal slots of the same source (reading Z8)
+__global__ void k_pos(const uint32_t* __restrict__ vals, const uint32_t* __restrict__ where,
+                      const uint32_t* __restrict__ nbr, const uint32_t* __restrict__ src,
+                      const uint32_t* __restrict__ off, uint64_t S, uint32_t* __restrict__ pos,
+                      uint32_t* __restrict__ flags) {
   for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < S; j += (uint64_t)gridDim.x * blockDim.x) {
-    uint32_t y = nbr[j], x = src[j];
-    if (j + 1 < off[x + 1] && nbr[j + 1] == y) atomicOr(flags, 2u);
-    uint32_t twin = where[vals[j] ^ 1u];
-    pos[j] = twin - off[y];
-    bool f = rkey[y] > rkey[x];
-    if (f) {
-      bool last = (j + 1 == off[x + 1]) || !(rkey[nbr[j + 1]] > rkey[x]);
-      if (last) hi[x] = (uint32_t)(j - off[x] + 1);
+    const uint32_t y = nbr[j];
+    if (j + 1 < S && nbr[j + 1] == y && src[j + 1] == src[j]) atomicOr(flags, 2u);
+    pos[j] = where[vals[j] ^ 1u] - off[y];
+  }
+}
+
+// hi[x] = deg_x(x) = #neighbours ranked above x: N(x) is one side, whose rid
+// order is its rank order, so they are a prefix of the row (decreasing rid);
+// binary search for its end
+__global__ void k_hi(const uint32_t* __restrict__ nbr, const uint32_t* __restrict__ off,
+                     const uint64_t* __restrict__ rkey, uint64_t n, uint32_t* __restrict__ hi) {
+  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < n; x += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t o = off[x];
+    uint32_t lo = 0, up = off[x + 1] - o;
+    const uint64_t kx = rkey[x];
+    while (lo < up) {
+      const uint32_t mid = (lo + up) >> 1;
+      if (rkey[nbr[o + mid]] > kx) lo = mid + 1;
+      else up = mid;
     }
+    hi[x] = lo;
   }
 }
 
@@ -440,7 +453,6 @@ bf_status graph_rank(bf_graph* g, int kind) {
   uint64_t* k1 = g->tmp_b.as<uint64_t>();
   uint32_t* v0 = g->tmp_c.as<uint32_t>();
   uint32_t* v1 = g->tmp_d.as<uint32_t>();
-  CUDA_TRY(cudaMemsetAsync(g->hi.p, 0, n1 * 4, s));
   g->dflag.ensure(16);
   CUDA_TRY(cudaMemsetAsync(g->dflag.p, 0, 4, s));
   if (m) {
@@ -458,9 +470,13 @@ bf_status graph_rank(bf_graph* g, int kind) {
                                     g->n_u, m, nbr + m, src + m, where, tmp, s, L);
     if (wu != wv) CUDA_TRY(cudaMemcpyAsync(wu ? v0 : v1, wu ? v1 : v0, m * 4, cudaMemcpyDeviceToDevice, s));
     uint32_t* vs = wv ? v1 : v0;  // slot ids in CSR order
-    k_pos_hi<<<grid_for(S, g->sms), TPB, 0, s>>>(vs, where, g->nbr.as<uint32_t>(), src, g->off.as<uint32_t>(),
-                                                  g->rkey.as<uint64_t>(), S, g->pos.as<uint32_t>(),
-                                                  g->hi.as<uint32_t>(), g->dflag.as<uint32_t>());
+    k_pos<<<grid_for(S, g->sms), TPB, 0, s>>>(vs, where, nbr, src, g->off.as<uint32_t>(), S, g->pos.as<uint32_t>(),
+                                               g->dflag.as<uint32_t>());
+    KERNEL_CHECK(g);
+  }
+  if (n) {
+    k_hi<<<grid_for(n, g->sms), TPB, 0, s>>>(g->nbr.as<uint32_t>(), g->off.as<uint32_t>(), g->rkey.as<uint64_t>(), n,
+                                              g->hi.as<uint32_t>());
     KERNEL_CHECK(g);
   }
   g->rank_kind = kind;
