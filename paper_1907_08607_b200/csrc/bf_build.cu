@@ -72,9 +72,11 @@ __global__ void k_side_sums(const uint32_t* __restrict__ deg, uint64_t n, uint32
   if (threadIdx.x < 2) atomicAdd(&sums[threadIdx.x], s[threadIdx.x]);
 }
 
-// sort key (side bit 31 | tier) and rank key per gid
-__global__ void k_rank_keys(const uint32_t* __restrict__ deg, uint64_t n, uint32_t nU, int kind,
-                            const unsigned long long* __restrict__ sums, uint32_t* __restrict__ skey,
+// sort key = side << tb | tier' with tier' in tb bits ordered as tier within
+// a side (degree: dmax - d; approximate degree: 63 - floor(log2 d) or 64; side
+// order: none), so the vertex sort runs over tb + 1 bits only
+__global__ void k_rank_keys(const uint32_t* __restrict__ deg, uint64_t n, uint32_t nU, int kind, int tb,
+                            uint32_t dmax, const unsigned long long* __restrict__ sums, uint32_t* __restrict__ skey,
                             uint32_t* __restrict__ iota, uint64_t* __restrict__ rkey_gid) {
   int u_first = kind == BF_RANK_SIDE ? (sums[0] <= sums[1]) : 1;
   for (uint64_t z = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; z < n; z += (uint64_t)gridDim.x * blockDim.x) {
@@ -84,7 +86,8 @@ __global__ void k_rank_keys(const uint32_t* __restrict__ deg, uint64_t n, uint32
     if (kind == BF_RANK_DEGREE) tier = 0x7FFFFFFFu - d;                           // decreasing degree
     else if (kind == BF_RANK_APPROX_DEGREE) tier = d ? 63u - (31u - __clz(d)) : 64u;  // decreasing floor(log2 d)
     else tier = (side == 0) == (u_first != 0) ? 0u : 1u;                          // first side, then the other
-    skey[z] = (side << 31) | (kind == BF_RANK_SIDE ? 0u : tier);
+    const uint32_t tc = kind == BF_RANK_SIDE ? 0u : kind == BF_RANK_DEGREE ? dmax - d : tier;
+    skey[z] = (side << tb) | tc;
     iota[z] = (uint32_t)z;
     rkey_gid[z] = ((uint64_t)tier << 32) | z;
   }
@@ -428,11 +431,17 @@ bf_status graph_rank(bf_graph* g, int kind) {
   if (n) {
     k_side_sums<<<grid_for(n, g->sms), TPB, 0, s>>>(g->deg.as<uint32_t>(), n, g->n_u, sums);
     KERNEL_CHECK(g);
-    k_rank_keys<<<grid_for(n, g->sms), TPB, 0, s>>>(g->deg.as<uint32_t>(), n, g->n_u, kind, sums, skey0, val0,
-                                                     rkey_gid);
+  }
+  // a vertex's degree is at most the other side's size
+  uint32_t dmax = std::max(g->n_u, g->n_v);
+  int tb = kind == BF_RANK_SIDE ? 0 : kind == BF_RANK_APPROX_DEGREE ? 7 : ceil_log2_u64((uint64_t)dmax + 1);
+  if (tb > 31) { tb = 31; dmax = 0x7FFFFFFFu; }  // degrees stay below 2^31 (m < 2^31 per vertex)
+  if (n) {
+    k_rank_keys<<<grid_for(n, g->sms), TPB, 0, s>>>(g->deg.as<uint32_t>(), n, g->n_u, kind, tb, dmax, sums, skey0,
+                                                     val0, rkey_gid);
     KERNEL_CHECK(g);
   }
-  int which = radix_sort_u32(skey0, val0, skey1, val1, n, 0, 32, tmp, s, L);
+  int which = radix_sort_u32(skey0, val0, skey1, val1, n, 0, tb + 1, tmp, s, L);
   uint32_t* gid_of_rid = which ? val1 : val0;
   if (gid_of_rid != g->gid_of_rid.as<uint32_t>() && n)
     CUDA_TRY(cudaMemcpyAsync(g->gid_of_rid.p, gid_of_rid, n * 4, cudaMemcpyDeviceToDevice, s));
