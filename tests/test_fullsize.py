@@ -75,7 +75,8 @@ def test_fullsize_sampled(k):
         for side, b, cost, deg in ((0, bu, cost_u, deg_u), (1, bv, cost_v, deg_v)):
             n_side = len(b)
             xs = list(rng.integers(0, n_side, 48))
-            hubs = [int(x) for x in np.argsort(-deg)[:64] if cost[x] <= ORACLE_STEP_BUDGET][:8]
+            by_deg = np.argsort(-deg)  # the highest-degree vertices the oracle can afford
+            hubs = [int(x) for x in by_deg[cost[by_deg] <= ORACLE_STEP_BUDGET][:8]]
             xs += hubs
             assert hubs, "no affordable hub sampled"
             for x in xs:

@@ -26,7 +26,7 @@ def main():
   cases = []
   for gspec in (["K", 40, 33], ["K", 17, 9], ["C", 1500, 900, 12000, 2.0, 2.3, 5]):
       for mode in ("total", "vertex", "edge"):
-          for flags in ([], ["FORCE_WARP"], ["FORCE_CTA"], ["FORCE_DENSE"], ["FORCE_DENSE", "SMALL_CHUNK"], ["SMALL_CHUNK"]):
+          for flags in ([], ["FORCE_WARP"], ["FORCE_CTA"], ["FORCE_DENSE"], ["FORCE_DENSE", "SMALL_CHUNK"], ["SMALL_CHUNK"], ["UNPACKED_SORT"]):
               for orient in ("high", "low"):
                   cases.append(dict(g=gspec, mode=mode, flags=flags, orient=orient, rank="degree"))
   for c in cases:
