@@ -172,7 +172,6 @@ __global__ void __launch_bounds__(RS_THREADS, BF_RS_MINB) k_rs_downsweep(const K
   __shared__ K skeys[RS_TILE];
   __shared__ uint32_t svals[VALS ? RS_TILE : 1];
   __shared__ __align__(16) uint32_t wcnt[RS_WARPS][256];
-  __shared__ uint32_t dstart[256];
   __shared__ uint32_t goff[256];
   __shared__ uint32_t wt[32];
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -213,14 +212,20 @@ __global__ void __launch_bounds__(RS_THREADS, BF_RS_MINB) k_rs_downsweep(const K
     run += c;
   }
   uint32_t tot;
-  dstart[tid] = block_exclusive_scan<uint32_t>(run, wt, &tot);
+  // fold the digit's tile start into its per-warp bases and its global offset
+  // (one shared lookup per key in each of the two scatters; u32 arithmetic
+  // wraps back into range since every position is < 2^32)
+  const uint32_t ds = block_exclusive_scan<uint32_t>(run, wt, &tot);
+#pragma unroll
+  for (int ww = 0; ww < RS_WARPS; ww++) wcnt[ww][tid] += ds;
+  goff[tid] -= ds;
   __syncthreads();
 #pragma unroll
   for (int r = 0; r < RS_ITEMS; r++) {
     size_t idx = tbase + (size_t)w * RS_WARP_SPAN + r * 32 + lane;
     if (idx < n) {
       uint32_t d = (uint32_t)(key[r] >> shift) & mask;
-      uint32_t p = dstart[d] + wcnt[w][d] + rk[r];
+      uint32_t p = wcnt[w][d] + rk[r];
       skeys[p] = key[r];
       if (VALS) svals[p] = val[r];
     }
@@ -233,7 +238,7 @@ __global__ void __launch_bounds__(RS_THREADS, BF_RS_MINB) k_rs_downsweep(const K
     for (uint32_t i = tid; i < cnt; i += RS_THREADS) {
       const uint64_t kr = (uint64_t)skeys[i];
       const uint32_t d = (uint32_t)(kr >> shift) & mask;
-      const size_t gp = (size_t)goff[d] + (i - dstart[d]);
+      const size_t gp = (uint32_t)(goff[d] + i);
       const uint64_t k = kr >> dec.Be;
       const uint32_t slot = VALS ? svals[i] : (uint32_t)(2 * (kr & emask) + dec.side);
       dec.nbr[gp] = (uint32_t)(dec.nbr_last - (k & lmask));
@@ -246,7 +251,7 @@ __global__ void __launch_bounds__(RS_THREADS, BF_RS_MINB) k_rs_downsweep(const K
   for (uint32_t i = tid; i < cnt; i += RS_THREADS) {
     K k = skeys[i];
     uint32_t d = (uint32_t)(k >> shift) & mask;
-    size_t gp = (size_t)goff[d] + (i - dstart[d]);
+    const size_t gp = (uint32_t)(goff[d] + i);
     kout[gp] = k;
     if (VALS) vout[gp] = svals[i];
   }
