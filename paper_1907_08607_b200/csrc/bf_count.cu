@@ -634,7 +634,7 @@ __device__ __forceinline__ void slots_pass2(const CountArgs& a, const Store& cs,
 #define BF_WARP_CACHE 0  // measured: the warp tier is faster re-reading keys through L1 (6.96 -> 6.85 ms)
 #endif
 #ifndef BF_MED_CACHE
-#define BF_MED_CACHE 1
+#define BF_MED_CACHE 0
 #endif
 #define SMALL_CACHE(NT) ((NT) == 32 ? (BF_WARP_CACHE != 0) : (BF_MED_CACHE != 0))
 
@@ -670,8 +670,11 @@ __device__ __forceinline__ SlotRegs load_slot(const CountArgs& a, uint32_t j, ui
   return r;
 }
 
+#ifndef BF_MED_MINB
+#define BF_MED_MINB 8
+#endif
 template <int ORIENT, int MODE, int NT, uint32_t WIN, uint32_t HS, uint32_t CAP, int P, int G, int UR>
-__global__ void __launch_bounds__(NT, 1) k_small(CountArgs a) {
+__global__ void __launch_bounds__(NT, NT == 32 ? 1 : BF_MED_MINB) k_small(CountArgs a) {
   using SM = SmallSmem<NT, WIN, HS, CAP, P, G, UR>;
   extern __shared__ __align__(16) char sm[];
   SM& ss = *(SM*)sm;
@@ -1004,8 +1007,10 @@ __global__ void __launch_bounds__(256) k_split_clear(CountArgs a, SplitArgs sa) 
 #ifndef BF_WARP_WIN
 #define BF_WARP_WIN 1024
 #endif
+// medium tier: (8192-key window, key cache, 6 CTAs/SM) -> (4096, no cache,
+// 8 CTAs/SM at <= 64 registers): c2 6.86 -> 6.63 ms, c3 84.5 -> 82.5 ms
 #ifndef BF_MED_WIN
-#define BF_MED_WIN 8192
+#define BF_MED_WIN 4096
 #endif
 #ifndef BF_BIG_WIN
 #define BF_BIG_WIN 4096
