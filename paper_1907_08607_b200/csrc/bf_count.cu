@@ -1043,7 +1043,10 @@ __global__ void __launch_bounds__(256) k_split_clear(CountArgs a, SplitArgs sa) 
 #define WARP_CFG 32, BF_WARP_WIN, 512, BF_WARP_MAX_WEDGES, BF_WARP_P, BF_WARP_G, BF_WARP_UR
 using WarpSM = SmallSmem<WARP_CFG>;
 // medium tier: 128 threads, w <= 2048, <= 128 slots
-#define MED_CFG BF_MEDIUM_MAX_SLOTS, BF_MED_WIN, 2048, BF_MEDIUM_MAX_WEDGES, BF_MED_P, BF_MED_G, BF_MED_UR
+#ifndef BF_MED_HS
+#define BF_MED_HS 2048
+#endif
+#define MED_CFG BF_MEDIUM_MAX_SLOTS, BF_MED_WIN, BF_MED_HS, BF_MEDIUM_MAX_WEDGES, BF_MED_P, BF_MED_G, BF_MED_UR
 using MedSM = SmallSmem<MED_CFG>;
 // heavy tier: 256 threads, chunks of <= 8192 wedges
 #ifndef BF_BIG_NT
