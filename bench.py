@@ -68,12 +68,13 @@ class ClockSampler:
     def __init__(self, gpu_index: int):
         self.idx = gpu_index
         self.proc = None
-        self.lines = []
+        self.lines = []  # (host arrival time, csv line)
+        self.windows = []  # timed regions (host time)
 
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -83,7 +84,10 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
+
+    def timed(self, t0: float, t1: float):
+        self.windows.append((t0, t1))
 
     def __exit__(self, *a):
         if self.proc:
@@ -94,9 +98,17 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
+        """Samples that arrived during a timed region (plus the sampling period,
+        as a sample reports the interval before it); if a region was shorter
+        than the period, the first sample after each region."""
         sm, smax, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        inside = [ln for t, ln in self.lines if any(a <= t <= b + 0.06 for a, b in self.windows)]
+        if not inside:
+            for a, b in self.windows:
+                after = [ln for t, ln in self.lines if t >= a]
+                inside += after[:1]
+        for ln in inside:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 9:
                 continue
@@ -111,7 +123,7 @@ class ClockSampler:
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
         return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": smax, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "period_ms": 50}
 
 
 # ----------------------------------------------------------------------------- CPU oracle
@@ -186,8 +198,19 @@ def algorithmic_bytes(mode: str, W: int, m: int, n: int, P: int) -> int:
     return 4 * W + 16 * m + 12 * n
 
 
-def load_traffic(cfg: int, mode: str, orient: str):
-    """dram bytes per launch of the wedge kernel from the committed ncu --set full summary."""
+def src_sha() -> str:
+    """SHA-256 over libbf's CUDA sources and header (ties a committed ncu profile to the code it measured)."""
+    import glob
+    import hashlib
+    h = hashlib.sha256()
+    for p in sorted(glob.glob(os.path.join(ROOT, "paper_1907_08607_b200", "csrc", "*"))) + \
+            [os.path.join(ROOT, "include", "bf.h")]:
+        h.update(open(p, "rb").read())
+    return h.hexdigest()[:16]
+
+
+def load_profile(cfg: int, mode: str, orient: str):
+    """The newest committed ncu --set full summary of the wedge kernels for this config and mode."""
     import glob
     for p in sorted(glob.glob(os.path.join(ROOT, "profiles", "*ncu_full*.json")), reverse=True):
         try:
@@ -195,8 +218,44 @@ def load_traffic(cfg: int, mode: str, orient: str):
         except Exception:
             continue
         if d.get("config") == cfg and d.get("mode") == mode and d.get("orient") == orient:
-            return d.get("dram_bytes_per_launch"), os.path.relpath(p, ROOT)
-    return None, None
+            d["path"] = os.path.relpath(p, ROOT)
+            d["matches"] = d.get("src_sha") == src_sha()
+            return d
+    return None
+
+
+def config_dict(a, g, W, rank_kind):
+    """The workload; identical in both arms (--impl ours / reference)."""
+    return {"workload": CONFIG_DESC[a.config] + f"; exact {a.mode} counts, {rank_kind} ranking",
+            "config": a.config, "n_u": g.n_u, "n_v": g.n_v, "m": g.m, "W": W, "ranking": rank_kind,
+            "mode": a.mode, "l2": "flushed between timed steps (256 MiB device write)",
+            "parallelism": f"dp{a.gpus}: wedge-prefix shares of one replicated ranked CSR, NCCL allreduce of outputs"}
+
+
+def check_parity(a, g, out_u, out_v, out_e, tot):
+    """SHA-256 of this run's outputs against the cached exact oracle outputs."""
+    import hashlib
+    try:
+        ref = json.load(open(os.path.join(ROOT, "tests", "golden", "fullsize_oracle.json"))).get(str(a.config))
+    except Exception:
+        ref = None
+    if not ref:
+        return {"status": "no cached oracle hash for this config"}
+    sha = lambda t: hashlib.sha256(t.cpu().numpy().view(np.uint64).astype("<u8").tobytes()).hexdigest()
+    e_sha = hashlib.sha256(np.ascontiguousarray(g.edges).astype("<u4").tobytes()).hexdigest()
+    if e_sha != ref["edges_sha256"]:
+        return {"status": "MISMATCH: the generated graph differs from the cached one"}
+    got = {"total": int(tot.cpu().numpy().view(np.uint64)[0])}
+    want = {"total": ref["total"]}
+    if a.mode == "vertex":
+        got.update(b_u=sha(out_u[:g.n_u]), b_v=sha(out_v[:g.n_v]))
+        want.update(b_u=ref["b_u_sha256"], b_v=ref["b_v_sha256"])
+    elif a.mode == "edge":
+        got["b_e"] = sha(out_e[:g.m])
+        want["b_e"] = ref["b_e_sha256"]
+    bad = [k for k in want if got[k] != want[k]]
+    return {"status": "sha256 match" if not bad else "MISMATCH: " + ",".join(bad),
+            "checked": sorted(want), "against": "tests/golden/fullsize_oracle.json (tools/oracle_cache.py)"}
 
 
 # ----------------------------------------------------------------------------- main
@@ -236,17 +295,14 @@ def main():
         except Exception as ex:  # the baseline is reported, never required
             cpu_base = {"value": None, "unit": UNIT, "cores": 0, "kind": "oracle", "sample": f"failed: {ex}"}
 
+    from paper_1907_08607_b200 import dist as bfd
     if world > 1:
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
         torch.cuda.set_device(0)
     dev = torch.device("cuda", local if world > 1 else 0)
-    comm = None
-    if world > 1:
-        uid = [bf.bf_nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
-        comm = bf.bf_nccl_comm_create(uid[0], rank, world, dev.index)
+    comm = bfd.nccl_comm_for_group(dev.index) if world > 1 else None
 
     stream = torch.cuda.current_stream(dev)
     orient = bf.ORIENTS[a.orient]
@@ -288,7 +344,7 @@ def main():
                 bf.bf_count_total(h, t)
             kms, cms, pairs = bf.bf_last_stats(h)
             return dict(W=bf.bf_wedge_count(h), kernel_ms=kms, count_ms=cms, pairs=pairs,
-                        launches=bf.bf_launch_count(h))
+                        launches=bf.bf_launch_count(h), shares=bf.bf_rank_shares(h, world) if world > 1 else None)
         finally:
             bf.bf_graph_destroy(h)
 
@@ -301,33 +357,39 @@ def main():
     for _ in range(max(a.warmup, 0)):
         info = step()
     torch.cuda.synchronize(dev)
-    W = info["W"] if info else step()["W"]
+    info = info or step()
+    W = info["W"]
+    shares = info["shares"]
 
     # timed region (device-resident inputs)
-    times, kms, launches, pairs = [], [], 0, []
+    times, kms, cms, launches, pairs = [], [], [], 0, []
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(dev.index) as clk:
+        time.sleep(0.3)  # nvidia-smi is up and sampling
         for _ in range(a.steps):
             flush.fill_(1)  # L2 flush between timed steps (256 MiB > 126 MB L2)
             torch.cuda.synchronize(dev)
             barrier()
+            h0 = time.time()
             ev0.record(stream)
             r = step()
             ev1.record(stream)
             torch.cuda.synchronize(dev)
+            clk.timed(h0, time.time())
             times.append(ev0.elapsed_time(ev1))
             kms.append(r["kernel_ms"])
+            cms.append(r["count_ms"])
             launches += r["launches"]
             pairs.append(r["pairs"])
     t_local = float(sum(times))
     t_kernel_local = float(np.mean(kms)) if kms else 0.0
-    if world > 1:
-        tt = torch.tensor([t_local, t_kernel_local], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_max, t_kernel = float(tt[0]), float(tt[1])
-    else:
-        t_max, t_kernel = t_local, t_kernel_local
+    t_count_local = float(np.mean(cms)) if cms else 0.0
+    t_max, t_kernel, t_count = bfd.max_over_ranks([t_local, t_kernel_local, t_count_local], device=dev)
     ms_step = t_max / max(a.steps, 1)
+
+    # self-check: the last step's outputs against the cached oracle SHA-256s
+    # (tests/golden/fullsize_oracle.json, written by tools/oracle_cache.py from oracle/ only)
+    parity = check_parity(a, g, out_u, out_v, out_e, tot)
 
     # end-to-end through the public API with host buffers (pinned), H2D + D2H inside
     e2e = None
@@ -348,11 +410,7 @@ def main():
             ev1.record(stream)
             torch.cuda.synchronize(dev)
             et.append(ev0.elapsed_time(ev1))
-        te = float(sum(et))
-        if world > 1:
-            tt = torch.tensor([te], dtype=torch.float64, device=dev)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            te = float(tt[0])
+        te = bfd.max_over_ranks([float(sum(et))], device=dev)[0]
         d2h = {"vertex": 8 * (n_u + n_v) + 8, "edge": 8 * m + 8, "total": 8}[a.mode]
         e2e = {"value": W * a.steps / (te / 1e3), "unit": UNIT, "h2d_bytes_per_step": 8 * m,
                "d2h_bytes_per_step": d2h, "ms_per_step": te / a.steps}
@@ -365,8 +423,9 @@ def main():
     value = W * a.steps / (t_max / 1e3)
     P = int(np.median(pairs)) if pairs else 0
     abytes = algorithmic_bytes(a.mode, W, m, n, P)
-    if world > 1:  # rank 0's share (the wedge prefix is split evenly)
-        abytes = algorithmic_bytes(a.mode, W // world, m // world, n // world, P)
+    if world > 1:  # rank 0's share (its wedges from the plan's deal; slots/vertices pro rata)
+        f0 = shares[0] / max(W, 1) if shares else 1.0 / world
+        abytes = algorithmic_bytes(a.mode, int(W * f0), int(m * f0), int(n * f0), P)
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -378,7 +437,9 @@ def main():
         peak, peak_src = 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
     achieved = abytes / (t_kernel / 1e3) / 1e9 if t_kernel > 0 else None
     orient_name = a.orient if a.orient != "auto" else "high"
-    traffic, traffic_src = load_traffic(a.config, a.mode, orient_name)
+    prof = load_profile(a.config, a.mode, orient_name)
+    traffic = prof.get("dram_bytes_per_launch") if prof else None
+    cfg = config_dict(a, g, W, rank_kind)
     out = {
         "metric": METRIC,
         "value": value,
@@ -392,30 +453,44 @@ def main():
         "vs_baseline": None,
         "dtype": "u32/u64",
         "data": "synthetic",
-        "config": {
-            "workload": CONFIG_DESC[a.config] + f"; exact {a.mode} counts, {rank_kind} ranking",
-            "config": a.config, "n_u": n_u, "n_v": n_v, "m": m, "W": W, "ranking": rank_kind,
-            "orient": orient_name, "mode": a.mode,
-            "step": "bf_graph_create + bf_rank + bf_count_* + destroy (SURVEY 8(a) a1-a9), edges resident in HBM",
-            "l2": "flushed between timed steps (256 MiB device write)",
-            "parallelism": f"dp{world}: wedge-prefix shares of one replicated ranked CSR, NCCL allreduce of outputs",
-        },
+        "config": cfg,
+        "step": "bf_graph_create + bf_rank + bf_count_* + destroy (SURVEY 8(a) a1-a9), edges resident in HBM",
         "edges_per_s": m * a.steps / (t_max / 1e3),
+        "phases_ms": {"t_count": t_count, "t_prep_and_destroy": ms_step - t_count,
+                      "note": "t_count = the whole bf_count_* call (CUDA events on the graph's stream, SURVEY 8(d)); "
+                              "t_prep = create + rank (ingest, ranking, ranked CSR, plan) + destroy"},
         "count_only": {"kernel_ms": t_kernel, "wedges_per_s": W / (t_kernel / 1e3) if t_kernel else None,
                        "edges_per_s": m / (t_kernel / 1e3) if t_kernel else None,
-                       "note": "wedge kernel alone (CUDA events around its launch on the graph's stream)"},
+                       "call_wedges_per_s": W / (t_count / 1e3) if t_count else None,
+                       "note": "kernel_ms: the wedge kernels alone (CUDA events around their launches on the "
+                               "graph's stream); call = t_count"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                     "frac_basis": "ALGORITHMIC bytes (SURVEY 8(d) model) / wedge-kernel time / measured HBM copy "
+                                   "peak; most re-reads hit L2, so actual DRAM traffic is far lower",
                      "kernel": "wedge kernels (k_split_walk/k_split_finalize, k_big, k_small x2) of one bf_count call",
                      "algorithmic_bytes": abytes, "P_pairs": P,
                      "bytes_model": {"vertex": "8W+48m+16P+28n", "edge": "28W+52m+12n",
                                      "total": "4W+16m+12n"}[a.mode],
-                     "peak_source": peak_src, "traffic_source": traffic_src},
+                     "peak_source": peak_src},
         "cpu_baseline": cpu_base,
         "e2e": e2e,
+        "parity": parity,
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }
+    if prof:
+        dram_gbs = traffic / (prof["kernel_ms"] / 1e3) / 1e9 if traffic and prof.get("kernel_ms") else None
+        out["roofline"]["measured"] = {
+            "source": prof["path"], "src_sha": prof.get("src_sha"), "matches_this_build": prof.get("matches"),
+            "dram_bytes_per_launch": traffic, "dram_gbs": dram_gbs,
+            "dram_frac": dram_gbs / peak if dram_gbs else None, "l2_hit_pct": prof.get("l2_hit_pct"),
+            "issue_active_pct": prof.get("issue_active_pct"), "warp_inst_per_wedge": prof.get("warp_inst_per_wedge"),
+            "limiter": prof.get("limiter")}
+        if not prof.get("matches"):
+            out["roofline"]["traffic"] = None  # the profile is of other code: report it beside, not as this run's
+    if world > 1:
+        out["shares"] = {"wedges_per_rank": shares, "max_over_mean": max(shares) * world / max(sum(shares), 1)}
     print(json.dumps(out), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -446,9 +521,9 @@ def run_reference(a, rank_kind):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
         "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "u64", "data": "synthetic",
-        "config": {"workload": CONFIG_DESC[a.config] + f"; exact {a.mode} counts, {rank_kind} ranking",
-                   "config": a.config, "n_u": g.n_u, "n_v": g.n_v, "m": g.m, "W": W, "ranking": rank_kind,
-                   "mode": a.mode},
+        "config": config_dict(a, g, W, rank_kind),
+        "ms_per_step_note": "extrapolated: each step times the oracle on a bounded sample of the workload "
+                            "(see cpu_baseline.sample) and scales by the oracle's step count",
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": last["cores"], "kind": "oracle",
                          "sample": last["sample"]},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},

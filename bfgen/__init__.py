@@ -20,6 +20,9 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SO = os.path.join(_HERE, "libbfgen.so")
+# bumped whenever bfgen.c or a CONFIGS entry changes the graphs it draws (keys the
+# cached full-size oracle hashes in tests/golden/fullsize_oracle.json)
+GEN_VERSION = 1
 _lib = None
 
 

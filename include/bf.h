@@ -21,7 +21,8 @@
  *    (e.g. on different devices) may be used concurrently.
  *  - Multi-GPU (bf_options.world_size > 1): every rank calls create, rank and
  *    count with identical inputs; bf_count_* is collective over nccl_comm and
- *    every rank receives the full result.
+ *    every rank receives the full result.  Whenever nccl_comm is set (a
+ *    1-rank communicator included) the outputs go through its allreduce.
  */
 #ifndef BF_H
 #define BF_H
@@ -73,7 +74,7 @@ typedef enum { BF_RANK_SIDE = 0, BF_RANK_APPROX_DEGREE = 1, BF_RANK_DEGREE = 2, 
 typedef enum { BF_ORIENT_AUTO = 0, BF_ORIENT_LOW = 1, BF_ORIENT_HIGH = 2 } bf_orient;
 
 /* test_flags bits (path forcing for tests; 0 in production).  Tiers of the
- * work plan: warp tier (w <= 512 wedges and <= 32 slots; per-warp u16 dense
+ * work plan: warp tier (w <= 512 wedges and <= 32 slots; per-warp u8 dense
  * key window + overflow hash), CTA medium tier (w <= 2048) and CTA heavy tier
  * (dense shared-memory key window + per-CTA global overflow row); heavy starts
  * above max(2^20, W / (8 * #SMs)) wedges are split into pieces counted by many
@@ -173,6 +174,14 @@ uint64_t bf_launch_count(const bf_graph* g);
  * use the same function.  Wedge-aware batching across GPUs. */
 uint64_t bf_deal_index(uint64_t q, int rank, int world, uint64_t t0, uint64_t t1);
 
+/* Multi-GPU work shares of the current plan (host output, after bf_rank):
+ * wedges[r] = the wedges rank r of `world` would process -- split starts
+ * whole, in snake order over their index, and every tier segment through
+ * bf_deal_index -- i.e. exactly the deal the kernels apply for
+ * bf_options.world_size = world.  wedges: `world` uint64 (host).
+ * Errors: BF_EINVAL, BF_ENORANK, BF_ECUDA. */
+bf_status bf_rank_shares(const bf_graph* g, int world, uint64_t* wedges);
+
 /* Debug/test export of the ranked CSR (device -> host copies).  Any pointer
  * may be NULL.  rid_of_gid[n]: rank-space id of global id gid (U-side vertices
  * occupy rid [0,n_u) in rank order, V-side [n_u, n) in rank order);
@@ -209,8 +218,32 @@ bf_status bf_nccl_comm_destroy(void* comm);
 bf_status bf_sparsify(uint32_t n_u, uint32_t n_v, const uint32_t* edges, uint64_t m, int method, double p,
                       uint64_t seed, uint32_t* out_edges, uint64_t* out_m, const bf_options* opt);
 
-/* Frees all device state of g (NULL is a no-op). */
+/* Approximate total count by sparsification, end to end on the device
+ * (P:1451-1493): bf_sparsify, then the kept graph through bf_graph_create,
+ * bf_rank(BF_RANK_AUTO) and bf_count_total (same options: device, stream,
+ * multi-GPU), then the unbiased scaling -- T_s / p^4 for BF_SPARSIFY_EDGE
+ * (each edge kept with probability p) and T_s * c^3 with
+ * c = ceil(1/p) colours for BF_SPARSIFY_COLOR (a butterfly survives iff its
+ * four vertices share a colour, probability c^-3; reading Z15).
+ * edges: host unless opt->edges_on_device.  estimate (host) receives the
+ * estimate; sparse_total / sparse_m (host, nullable) the exact count and the
+ * edge count of the sparsified graph.  Errors: as bf_sparsify, bf_rank and
+ * bf_count_total. */
+bf_status bf_approx_total(uint32_t n_u, uint32_t n_v, const uint32_t* edges, uint64_t m, int method, double p,
+                          uint64_t seed, const bf_options* opt, double* estimate, uint64_t* sparse_total,
+                          uint64_t* sparse_m);
+
+/* Frees all device state of g (NULL is a no-op).  Freed device memory goes
+ * back to the library's private per-device pool (not the device's default
+ * pool), so the next graph reuses it; see bf_release_device_cache. */
 void bf_graph_destroy(bf_graph* g);
+
+/* Returns the library's cached device memory on `device` to the driver: the
+ * heavy tier's per-CTA overflow rows (kept zero across calls and graphs, up
+ * to 16 GB) and the unused blocks of the private stream-ordered pool.  Safe at
+ * any time (a later count reallocates what it needs); synchronises the device.
+ * Errors: BF_EINVAL (bad device), BF_ECUDA. */
+bf_status bf_release_device_cache(int device);
 
 const char* bf_status_str(bf_status s);
 const char* bf_last_error(void);

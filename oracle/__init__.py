@@ -26,7 +26,7 @@ _SO = os.path.join(_HERE, "liboracle.so")
 _lib = None
 
 ORC_ERRORS = {1: "ERANGE", 2: "EDUP", 3: "ENOMEM", 4: "EOVERFLOW", 5: "EINVAL"}
-RANK_KINDS = {"side": 0, "approx_degree": 1, "degree": 2, "explicit": 3}
+RANK_KINDS = {"side": 0, "approx_degree": 1, "degree": 2, "explicit": 3, "approx_codegen": 4}
 
 
 class OracleError(RuntimeError):
@@ -144,6 +144,88 @@ class OracleGraph:
         if a["total"] != b["total"]:
             raise OracleError("side-0 and side-1 totals disagree")
         return a
+
+    def count_sharded(self, procs: int | None = None, side: int | None = None, vertex=True, edge=True):
+        """The same exact counts as ``count``, computed by ``procs`` forked
+        single-threaded workers over disjoint x-ranges of the enumeration side X
+        (SURVEY 8(c) step 7).  b(x) and b(e) (edges grouped by their X endpoint)
+        are disjoint per shard and written in place into shared memory; the
+        centre-rule partials b(y) overlap and are summed here, exactly (u64 with
+        a carry check; the C code checks each shard's values).  Shards are cut
+        at equal cost sum_{y in N(x)} deg(y), so they finish together."""
+        import mmap
+        import multiprocessing as mp
+
+        X = self.cheap_side() if side is None else side
+        Y = 1 - X
+        nX, nY = self.n[X], self.n[Y]
+        P = max(1, int(procs or len(os.sched_getaffinity(0))))
+        deg_y = np.bincount(self.edges[:, Y], minlength=nY).astype(np.float64)
+        cost = np.bincount(self.edges[:, X], weights=deg_y[self.edges[:, Y]], minlength=nX) + 1.0
+        csum = np.cumsum(cost)
+        cuts = np.searchsorted(csum, np.linspace(0, csum[-1], P + 1)[1:-1]) if nX else np.zeros(0, np.int64)
+        bounds = list(zip([0] + [int(c) for c in cuts], [int(c) for c in cuts] + [nX]))
+        P = len(bounds)
+
+        def shared(nelem):
+            buf = mmap.mmap(-1, max(nelem, 1) * 8)
+            return buf, np.frombuffer(buf, np.uint64, count=max(nelem, 1))
+
+        keep = []
+        bx = by = be = None
+        if vertex:
+            b1, bx = shared(nX)
+            b2, by = shared(P * nY)
+            by = by[:P * nY].reshape(P, nY) if nY else np.zeros((P, 0), np.uint64)
+            keep += [b1, b2]
+        if edge:
+            b3, be = shared(self.m)
+            keep.append(b3)
+        b4, sums = shared(P)
+        b5, rcs = shared(P)
+        keep += [b4, b5]
+
+        def work(i):
+            lo, hi = bounds[i]
+            s = ctypes.c_uint64(0)
+            rc = self.lib.orc_count(self.h, X, lo, hi, _p64(bx) if vertex else None,
+                                    _p64(by[i]) if vertex and nY else None, _p64(be) if edge else None,
+                                    ctypes.byref(s))
+            sums[i] = s.value
+            rcs[i] = rc
+
+        import warnings
+        ctx = mp.get_context("fork")
+        ps = [ctx.Process(target=work, args=(i,)) for i in range(P)]
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore", DeprecationWarning)  # the workers only call the C oracle
+            for p in ps:
+                p.start()
+        for p in ps:
+            p.join()
+        if any(p.exitcode != 0 for p in ps):
+            raise OracleError("oracle shard died")
+        for rc in rcs[:P]:
+            _check(int(rc))
+        total2 = sum(int(s) for s in sums[:P])
+        if total2 >= 1 << 64:
+            raise OracleError("EOVERFLOW")
+        if total2 % 2:
+            raise OracleError("sum of b(x) over a side is odd")
+        out_y = None
+        if vertex:
+            out_y = np.zeros(nY, np.uint64)
+            for i in range(P):
+                nxt = out_y + by[i]
+                if (nxt < out_y).any():
+                    raise OracleError("EOVERFLOW")
+                out_y = nxt
+            bx = np.array(bx[:nX])
+        if edge:
+            be = np.array(be[:self.m])
+        del keep
+        b_u, b_v = (bx, out_y) if X == 0 else (out_y, bx)
+        return dict(total=total2 // 2, b_u=b_u, b_v=b_v, b_e=be, side=X, shards=P)
 
     def vertex(self, side: int, x: int) -> int:
         out = ctypes.c_uint64(0)

@@ -223,19 +223,65 @@ int orc_edge(orc_graph* g, const uint32_t* edges, uint64_t e, uint64_t* out) {
  *                   (readings Z2, Z3).
  *   kind 2 degree:  decreasing degree, ties by gid (reading Z2).
  *   kind 3 explicit: rank_out is an input (a permutation), left as is.
+ *   kind 4 approximate complement degeneracy:
+ *                   "repeatedly removes vertices of largest log-degree" --
+ *                   each round removes ALL remaining vertices whose
+ *                   floor(log2 of the degree in the subgraph induced on the
+ *                   remaining vertices) equals the current maximum (deg 0 ->
+ *                   -1), then lowers their remaining neighbours' degrees;
+ *                   vertices removed in earlier rounds rank first, ties by
+ *                   gid (readings Z2, Z3, Z16).
  * --------------------------------------------------------------------- */
+static int64_t floor_log2(uint64_t d) { int64_t l = -1; while (d) { l++; d >>= 1; } return l; }
+static int rank_approx_codegen(const orc_graph* g, uint32_t* rank_out) {
+  uint64_t nU = g->n[0], n = nU + g->n[1];
+  uint64_t* cur = (uint64_t*)malloc((n ? n : 1) * 8);
+  uint8_t* alive = (uint8_t*)malloc(n ? n : 1);
+  uint8_t* dying = (uint8_t*)malloc(n ? n : 1);
+  if (!cur || !alive || !dying) { free(cur); free(alive); free(dying); return ORC_ENOMEM; }
+  for (uint64_t z = 0; z < n; z++) {
+    cur[z] = z < nU ? orc_degree(g, 0, (uint32_t)z) : orc_degree(g, 1, (uint32_t)(z - nU));
+    alive[z] = 1;
+  }
+  uint64_t next = 0, left = n;
+  while (left) {
+    int64_t B = -2;
+    for (uint64_t z = 0; z < n; z++)
+      if (alive[z] && floor_log2(cur[z]) > B) B = floor_log2(cur[z]);
+    for (uint64_t z = 0; z < n; z++) {  /* this round's vertices, in gid order */
+      dying[z] = alive[z] && floor_log2(cur[z]) == B;
+      if (dying[z]) rank_out[z] = (uint32_t)next++;
+    }
+    for (uint64_t z = 0; z < n; z++) {
+      if (!dying[z]) continue;
+      alive[z] = 0;
+      left--;
+    }
+    for (uint64_t z = 0; z < n; z++) {  /* remaining neighbours lose the removed vertices */
+      if (!dying[z]) continue;
+      int X = z < nU ? 0 : 1, Y = 1 - X;
+      uint32_t x = (uint32_t)(X ? z - nU : z);
+      for (uint64_t i = g->off[X][x]; i < g->off[X][x + 1]; i++) {
+        uint64_t gy = Y ? nU + g->adj[X][i] : g->adj[X][i];
+        if (alive[gy]) cur[gy]--;
+      }
+    }
+  }
+  free(cur); free(alive); free(dying);
+  return ORC_OK;
+}
 static int64_t* g_sort_key; /* qsort comparator context (single-threaded) */
 static int cmp_by_key(const void* a, const void* b) {
   uint32_t x = *(const uint32_t*)a, y = *(const uint32_t*)b;
   if (g_sort_key[x] != g_sort_key[y]) return g_sort_key[x] > g_sort_key[y] ? -1 : 1; /* decreasing key */
   return x < y ? -1 : x > y; /* ties: increasing gid */
 }
-static int64_t floor_log2(uint64_t d) { int64_t l = -1; while (d) { l++; d >>= 1; } return l; }
 
 int orc_rank(const orc_graph* g, int kind, uint32_t* rank_out) {
   uint64_t nU = g->n[0], n = (uint64_t)g->n[0] + g->n[1];
   if (kind == 3) return ORC_OK;
-  if (kind < 0 || kind > 3) return ORC_EINVAL;
+  if (kind == 4) return rank_approx_codegen(g, rank_out);
+  if (kind < 0 || kind > 4) return ORC_EINVAL;
   int64_t* key = (int64_t*)malloc((n ? n : 1) * 8);
   uint32_t* order = (uint32_t*)malloc((n ? n : 1) * 4);
   if (kind == 0) {

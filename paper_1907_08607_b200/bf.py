@@ -60,10 +60,15 @@ _sig = {
     "bf_deal_index": (ctypes.c_uint64, [ctypes.c_uint64, ctypes.c_int, ctypes.c_int, ctypes.c_uint64,
                                         ctypes.c_uint64]),
     "bf_export_csr": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "bf_rank_shares": (ctypes.c_int, [_vp, ctypes.c_int, _u64p]),
+    "bf_approx_total": (ctypes.c_int, [ctypes.c_uint32, ctypes.c_uint32, _vp, ctypes.c_uint64, ctypes.c_int,
+                                       ctypes.c_double, ctypes.c_uint64, ctypes.POINTER(bf_options),
+                                       ctypes.POINTER(ctypes.c_double), _u64p, _u64p]),
     "bf_nccl_unique_id": (ctypes.c_int, [_vp]),
     "bf_nccl_comm_create": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_vp)]),
     "bf_nccl_comm_destroy": (ctypes.c_int, [_vp]),
     "bf_graph_destroy": (None, [_vp]),
+    "bf_release_device_cache": (ctypes.c_int, [ctypes.c_int]),
     "bf_status_str": (ctypes.c_char_p, [ctypes.c_int]),
     "bf_last_error": (ctypes.c_char_p, []),
 }
@@ -171,15 +176,26 @@ def bf_sparsify(n_u: int, n_v: int, edges, method, p: float, seed: int, opt: bf_
     return out[:int(k.value)]
 
 
-def approx_total(n_u: int, n_v: int, edges, p: float, method="edge", seed: int = 0, rank="auto", **opts) -> float:
-    """Unbiased estimate of the total butterfly count: sparsify on the device,
-    count the kept graph exactly, scale by p^-4 (edge) or ceil(1/p)^3 (colour)."""
-    kept = bf_sparsify(n_u, n_v, edges, method, p, seed)
-    with ButterflyGraph(n_u, n_v, kept, rank=rank, **opts) as bg:
-        t = bg.total()
-    if (SPARSIFY_METHODS[method] if isinstance(method, str) else int(method)) == BF_SPARSIFY_EDGE:
-        return t / p ** 4
-    return t * float(np.ceil(1.0 / p)) ** 3
+def bf_approx_total(n_u: int, n_v: int, edges, method, p: float, seed: int = 0, opt: bf_options | None = None):
+    """Approximate total count by sparsification, all in libbf.
+    Returns (estimate, exact count of the sparsified graph, its edge count)."""
+    o = opt if opt is not None else bf_options_default()
+    if _on_device(edges):
+        o.edges_on_device = 1
+        m = int(edges.numel() // 2)
+    else:
+        edges = np.ascontiguousarray(edges, dtype=np.uint32).reshape(-1, 2)
+        m = edges.shape[0]
+    est, t, km = ctypes.c_double(0), ctypes.c_uint64(0), ctypes.c_uint64(0)
+    mth = SPARSIFY_METHODS[method] if isinstance(method, str) else int(method)
+    _check(_lib.bf_approx_total(n_u, n_v, _ptr(edges), m, mth, float(p), int(seed) & (2**64 - 1), ctypes.byref(o),
+                                ctypes.byref(est), ctypes.byref(t), ctypes.byref(km)), "bf_approx_total")
+    return float(est.value), int(t.value), int(km.value)
+
+
+def approx_total(n_u: int, n_v: int, edges, p: float, method="edge", seed: int = 0) -> float:
+    """Unbiased estimate of the total butterfly count (bf_approx_total)."""
+    return bf_approx_total(n_u, n_v, edges, method, p, seed)[0]
 
 
 def bf_last_stats(g):
@@ -195,6 +211,13 @@ def bf_launch_count(g) -> int:
 
 def bf_deal_index(q: int, rank: int, world: int, t0: int, t1: int) -> int:
     return int(_lib.bf_deal_index(q, rank, world, t0, t1))
+
+
+def bf_rank_shares(g, world: int) -> list[int]:
+    """Wedges each of `world` ranks would process under the current plan."""
+    w = (ctypes.c_uint64 * max(world, 1))()
+    _check(_lib.bf_rank_shares(g, world, w), "bf_rank_shares")
+    return [int(x) for x in w[:world]]
 
 
 def bf_export_csr(g, n: int, m: int):
@@ -227,6 +250,10 @@ def bf_nccl_comm_destroy(comm) -> None:
 
 def bf_graph_destroy(g) -> None:
     _lib.bf_graph_destroy(g)
+
+
+def bf_release_device_cache(device: int = 0) -> None:
+    _check(_lib.bf_release_device_cache(device), "bf_release_device_cache")
 
 
 class ButterflyGraph:

@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <mutex>
 #include <new>
+#include <vector>
 
 static thread_local char g_err[512] = "";
 
@@ -22,7 +23,8 @@ void bf_set_error(const char* fmt, ...) {
 void DevBuf::ensure(size_t n) {
   if (n <= bytes && p) return;
   if (p) { CUDA_TRY(cudaFreeAsync(p, s)); p = nullptr; bytes = 0; }
-  CUDA_TRY(cudaMallocAsync(&p, n, s));
+  if (pool) CUDA_TRY(cudaMallocFromPoolAsync(&p, n, pool, s));
+  else CUDA_TRY(cudaMallocAsync(&p, n, s));
   bytes = n;
 }
 void DevBuf::release() {
@@ -65,6 +67,38 @@ struct DeviceGuard {
   }
 };
 
+namespace {
+struct DeviceState {
+  int graphs = 0;
+  cudaMemPool_t pool = nullptr;
+};
+std::mutex g_dev_mu;
+DeviceState g_dev[64];
+}  // namespace
+
+cudaMemPool_t device_attach(int dev) {
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  DeviceState& d = g_dev[dev & 63];
+  if (!d.pool) {
+    cudaMemPoolProps props;
+    memset(&props, 0, sizeof(props));
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    CUDA_TRY(cudaMemPoolCreate(&d.pool, &props));
+    uint64_t keep = UINT64_MAX;
+    CUDA_TRY(cudaMemPoolSetAttribute(d.pool, cudaMemPoolAttrReleaseThreshold, &keep));
+  }
+  d.graphs++;
+  return d.pool;
+}
+
+void device_detach(int dev) {
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  DeviceState& d = g_dev[dev & 63];
+  if (d.graphs > 0) d.graphs--;
+}
+
 extern "C" {
 
 void bf_options_default(bf_options* opt) {
@@ -100,6 +134,7 @@ void bf_graph_destroy(bf_graph* g) {
   for (auto& e : g->ev)
     if (e) cudaEventDestroy(e);
   if (g->own_stream && g->stream) cudaStreamDestroy(g->stream);
+  if (g->attached) device_detach(g->device);
   delete g;
 }
 
@@ -138,13 +173,10 @@ bf_status bf_graph_create(uint32_t n_u, uint32_t n_v, const uint32_t* edges, uin
       g->own_stream = true;
     }
     for (auto& e : g->ev) CUDA_TRY(cudaEventCreate(&e));
-    // stream-ordered allocations from the device's default pool; keep freed
-    // blocks cached so repeated create/destroy does not return to the driver
-    cudaMemPool_t pool;
-    CUDA_TRY(cudaDeviceGetDefaultMemPool(&pool, g->device));
-    uint64_t keep = UINT64_MAX;
-    CUDA_TRY(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
-    g->for_each_buf([&](DevBuf& b) { b.s = g->stream; });
+    cudaMemPool_t pool = device_attach(g->device);
+    g->attached = true;
+    g->for_each_buf([&](DevBuf& b) { b.s = g->stream; b.pool = pool; });
+    NvtxRange r("bf a1 ingest");
     return graph_ingest(g, edges);
   });
   if (st != BF_OK) {
@@ -162,8 +194,13 @@ bf_status bf_rank(bf_graph* g, bf_rank_kind kind) {
   DeviceGuard dg(g->device);
   g->ranked = false;
   bf_status st = guarded(g, [&]() -> bf_status {
-    bf_status s = graph_rank(g, kind);
+    bf_status s;
+    {
+      NvtxRange r("bf a2-a3 rank + ranked CSR");
+      s = graph_rank(g, kind);
+    }
     if (s != BF_OK) return s;
+    NvtxRange r("bf a4 wedge prefix + plan");
     return graph_plan(g);
   });
   if (st == BF_OK) g->ranked = true;
@@ -226,6 +263,58 @@ uint64_t bf_launch_count(const bf_graph* g) { return g ? g->launches : 0; }
 uint64_t bf_deal_index(uint64_t q, int rank, int world, uint64_t t0, uint64_t t1) {
   if (world < 1 || rank < 0 || rank >= world || t1 < t0) return t1;
   return bf_deal(q, (uint64_t)rank, (uint64_t)world, t0, t1);
+}
+
+bf_status bf_release_device_cache(int device) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || device < 0 || device >= n) {
+    cudaGetLastError();
+    bf_set_error("bad device");
+    return BF_EINVAL;
+  }
+  DeviceGuard dg(device);
+  cudaSetDevice(device);
+  row_pool_free(device);  // takes the pool's lock: never under a running count
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  DeviceState& d = g_dev[device & 63];
+  if (d.pool) {
+    if (cudaDeviceSynchronize() != cudaSuccess || cudaMemPoolTrimTo(d.pool, 0) != cudaSuccess) {
+      bf_set_error("CUDA error while trimming the pool");
+      return BF_ECUDA;
+    }
+  }
+  return BF_OK;
+}
+
+bf_status bf_rank_shares(const bf_graph* g, int world, uint64_t* wedges) {
+  if (!g || !wedges || world < 1) { bf_set_error("bad argument"); return BF_EINVAL; }
+  if (!g->ranked) { bf_set_error("bf_rank has not been called"); return BF_ENORANK; }
+  DeviceGuard dg(g->device);
+  bf_graph* gg = const_cast<bf_graph*>(g);
+  return guarded(gg, [&]() -> bf_status {
+    const uint32_t nnz = g->n_tier[0] + g->n_tier[1] + g->n_tier[2];
+    std::vector<uint4> items(nnz);
+    std::vector<uint64_t> ws(g->n);
+    if (nnz) CUDA_TRY(cudaMemcpyAsync(items.data(), g->items.p, (size_t)nnz * 16, cudaMemcpyDeviceToHost, g->stream));
+    if (g->n) CUDA_TRY(cudaMemcpyAsync(ws.data(), g->wstart.p, g->n * 8, cudaMemcpyDeviceToHost, g->stream));
+    CUDA_TRY(cudaStreamSynchronize(g->stream));
+    for (int r = 0; r < world; r++) wedges[r] = 0;
+    // split starts: whole starts, snake order over their index (k_split_walk's split_mine)
+    for (uint32_t i = 0; i < g->n_split; i++) {
+      const uint32_t q = i / (uint32_t)world, r = i % (uint32_t)world;
+      wedges[(q & 1u) ? world - 1 - r : r] += ws[items[i].x];
+    }
+    // tier segments: the kernels' deal (bf_deal)
+    const uint32_t seg[4] = {g->n_split, g->n_tier[0], g->n_tier[0] + g->n_tier[1], nnz};
+    for (int t = 0; t < 3; t++)
+      for (int r = 0; r < world; r++)
+        for (uint64_t q = 0;; q++) {
+          const uint64_t i = bf_deal(q, (uint64_t)r, (uint64_t)world, seg[t], seg[t + 1]);
+          if (i >= seg[t + 1]) break;
+          wedges[r] += ws[items[i].x];
+        }
+    return BF_OK;
+  });
 }
 
 bf_status bf_export_csr(const bf_graph* g, uint32_t* rid_of_gid, uint32_t* off, uint32_t* nbr, uint32_t* pos,

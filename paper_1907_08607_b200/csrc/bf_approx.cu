@@ -116,3 +116,54 @@ extern "C" bf_status bf_sparsify(uint32_t n_u, uint32_t n_v, const uint32_t* edg
   if (prev >= 0) cudaSetDevice(prev);
   return st;
 }
+
+// Sparsify on the device, count the kept graph exactly through the same path
+// (create, rank, count_total; the caller's options, so multi-GPU works), and
+// scale into the estimator of P:1462-1479: edge sparsification keeps each edge
+// with probability p, so E[T_s] = p^4 T and T_s / p^4 is unbiased; colourful
+// sparsification keeps a butterfly iff its four vertices share a colour,
+// probability c^-3 with c = ceil(1/p) colours (reading Z15: the paper writes
+// "p^3"; c^3 is the unbiased factor when 1/p is not an integer).
+extern "C" bf_status bf_approx_total(uint32_t n_u, uint32_t n_v, const uint32_t* edges, uint64_t m, int method,
+                                     double p, uint64_t seed, const bf_options* opt, double* estimate,
+                                     uint64_t* sparse_total, uint64_t* sparse_m) {
+  if (!estimate) { bf_set_error("estimate is NULL"); return BF_EINVAL; }
+  bf_options o;
+  if (opt) o = *opt; else bf_options_default(&o);
+  const uint64_t m1 = m ? m : 1;
+  void* d_kept = nullptr;
+  int prev = -1;
+  cudaGetDevice(&prev);
+  if (cudaSetDevice(o.device) != cudaSuccess || cudaMalloc(&d_kept, m1 * 8) != cudaSuccess) {
+    cudaGetLastError();
+    if (prev >= 0) cudaSetDevice(prev);
+    bf_set_error("out of device memory");
+    return BF_ENOMEM;
+  }
+  bf_options so = o;
+  so.outputs_on_device = 1;  // kept edges stay on the device
+  uint64_t km = 0;
+  bf_status st = bf_sparsify(n_u, n_v, edges, m, method, p, seed, (uint32_t*)d_kept, &km, &so);
+  uint64_t t = 0;
+  if (st == BF_OK) {
+    bf_options co = o;
+    co.edges_on_device = 1;
+    co.outputs_on_device = 0;  // the total comes back to the host
+    bf_graph* g = nullptr;
+    st = bf_graph_create(n_u, n_v, (const uint32_t*)d_kept, km, &co, &g);
+    if (st == BF_OK) st = bf_rank(g, BF_RANK_AUTO);
+    if (st == BF_OK) st = bf_count_total(g, &t);
+    bf_graph_destroy(g);
+  }
+  cudaFree(d_kept);
+  if (prev >= 0) cudaSetDevice(prev);
+  if (st != BF_OK) return st;
+  if (sparse_total) *sparse_total = t;
+  if (sparse_m) *sparse_m = km;
+  if (method == BF_SPARSIFY_EDGE) *estimate = (double)t / (p * p * p * p);
+  else {
+    const double c = ceil(1.0 / p);
+    *estimate = (double)t * c * c * c;
+  }
+  return BF_OK;
+}

@@ -255,6 +255,7 @@ struct TierRule {
   uint64_t tl, tm;       // warp tier: w <= tl and slots <= ts; medium: w <= tm and slots <= ms
   uint32_t ts, ms;
   int no_warp, all_heavy;
+  uint32_t nU;           // side boundary (key range of a start)
 };
 
 __global__ void k_order_keys(const uint64_t* __restrict__ wstart, const uint32_t* __restrict__ off,
@@ -276,13 +277,22 @@ __global__ void k_order_keys(const uint64_t* __restrict__ wstart, const uint32_t
       const uint32_t wc = (uint32_t)(w > 0x3FFFFFFFull ? 0x3FFFFFFFull : w);
       key[r] = (tier << 30) | (0x3FFFFFFFu - wc);
     }
+    // key range of a heavy start: same-side rids ranked above it (HIGH) or
+    // below it (LOW); the heavy tier's per-CTA rows are sized by the maximum
+    uint32_t kr = 0;
+    if (tier == 0) {
+      const uint64_t hi_side = r < tr.nU ? tr.nU : n;
+      kr = (uint32_t)(orient == BF_ORIENT_LOW ? hi_side - r - 1 : (r < tr.nU ? r : r - tr.nU));
+    }
     const uint32_t a = __popc(__ballot_sync(0xffffffffu, w > 0));
     const uint32_t b = __popc(__ballot_sync(0xffffffffu, tier == 0));
     const uint32_t c = __popc(__ballot_sync(0xffffffffu, tier == 1));
+    const uint32_t kmax = __reduce_max_sync(0xffffffffu, kr);
     if ((threadIdx.x & 31) == 0) {
       if (a) atomicAdd(&cnts[0], a);
       if (b) atomicAdd(&cnts[1], b);
       if (c) atomicAdd(&cnts[2], c);
+      if (kmax) atomicMax(&cnts[3], kmax);
     }
   }
 }
@@ -529,6 +539,7 @@ bf_status graph_plan(bf_graph* g) {
   tr.ms = BF_MEDIUM_MAX_SLOTS;
   tr.no_warp = (g->opt.test_flags & BF_FLAG_FORCE_CTA) != 0;
   tr.all_heavy = (g->opt.test_flags & BF_FLAG_FORCE_DENSE) != 0;
+  tr.nU = g->n_u;
   if (g->opt.test_flags & BF_FLAG_FORCE_WARP) tr.tm = tr.tl;
   g->t1 = (uint32_t)tr.tl;
   g->t2 = (uint32_t)tr.tm;
@@ -552,9 +563,9 @@ bf_status graph_plan(bf_graph* g) {
     KERNEL_CHECK(g);
   }
   uint64_t host = 0;
-  uint32_t hc[3], hflag = 0;
+  uint32_t hc[4], hflag = 0;
   CUDA_TRY(cudaMemcpyAsync(&host, dW, 8, cudaMemcpyDeviceToHost, s));
-  CUDA_TRY(cudaMemcpyAsync(hc, cnts, 12, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaMemcpyAsync(hc, cnts, 16, cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaMemcpyAsync(&hflag, g->dflag.p, 4, cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaStreamSynchronize(s));
   if (hflag & 2u) { bf_set_error("duplicate edge"); return BF_EDUP; }
@@ -563,6 +574,7 @@ bf_status graph_plan(bf_graph* g) {
   g->n_tier[0] = hc[1];
   g->n_tier[1] = hc[2];
   g->n_tier[2] = nnz - hc[1] - hc[2];
+  g->heavy_keys = hc[3] + 1;  // key offsets of heavy starts are < this
   int w = radix_sort_u32(k0, v0, k1, g->order.as<uint32_t>(), nnz, 0, 32, tmp, s, L);
   if (!w && nnz) CUDA_TRY(cudaMemcpyAsync(g->order.p, v0, (size_t)nnz * 4, cudaMemcpyDeviceToDevice, s));
   g->items.ensure((size_t)std::max<uint32_t>(nnz, 1) * 16);

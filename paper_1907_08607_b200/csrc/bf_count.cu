@@ -31,17 +31,17 @@
 //
 // Tiers (wedge-aware batching) over one list of starts sorted by
 // (tier, wedges desc), dealt to ranks in snake order:
-//   warp   (w <= 512, <= 32 slots): one warp per start; u16 dense key window in
+//   warp   (w <= 512, <= 32 slots): one warp per start; u8 dense key window in
 //          shared memory (north_star "shared-memory ... keyed by u2") with an
-//          open-addressed shared hash for keys past the window; the start's
-//          keys are cached in shared memory for pass 2;
+//          open-addressed shared hash for keys past the window; pass 2 re-reads
+//          the keys through L1;
 //   medium (w <= 2048, <= 128 slots): one 128-thread CTA per start, same
-//          structures at CTA scope, owners marked by per-wedge bits;
+//          structures at CTA scope;
 //   heavy  (the rest): one 256-thread CTA per start, u32 dense shared window +
 //          a per-CTA global dense overflow row (north_star "dense per-CTA
-//          counter array"); starts that fit one chunk (<= 4096 wedges) cache
-//          their keys and owner bits on chip, larger ones are walked chunk by
-//          chunk with a global touched list.
+//          counter array"); starts of one chunk (<= 32768 wedges) reuse their
+//          unit table in pass 2, larger ones are walked chunk by chunk with a
+//          global touched list.
 // Counters are reset through the owners (the wedge whose increment took a
 // counter from 0 to 1), never by clearing whole rows.
 #include "bf_internal.h"
@@ -68,13 +68,12 @@ struct CountArgs {
   uint64_t* total;        // [0] total, [1] distinct pairs
   uint32_t* orow;         // heavy: per-CTA overflow rows (indexed by key offset)
   uint32_t* olist;        // heavy: per-CTA touched lists (multi-chunk starts)
-  uint64_t orow_len;       // heavy overflow row length (max side size - heavy window)
-  uint64_t olist_len;      // heavy touched-list capacity beyond the shared list (max side size)
+  uint64_t orow_len;       // heavy overflow row length (max heavy key range - heavy window)
+  uint64_t olist_len;      // heavy touched-list capacity beyond the shared list (max heavy key range)
   uint32_t* queue;        // tier cursor
   uint32_t n_u, n_v;
   uint32_t t0, t1;        // this tier's segment of the item list
   uint64_t S, n;          // slots, vertices (bounds checks of the debug build)
-  uint32_t dbg_stop;      // debug build: stop each start after this phase (0 = never)
   uint32_t exp;           // libbf_prof.so only: timing experiments (env BF_EXPERIMENT; results are wrong when set):
                           // 1 = skip endpoint REDs, 2 = skip centre REDs
   uint32_t win;           // dense window keys in use (<= compile-time size)
@@ -1068,6 +1067,15 @@ using MedSM = SmallSmem<MED_CFG>;
 constexpr uint64_t HV_WIN_KEYS = BF_BIG_WIN;  // BIG_CFG's window
 using BigSM = HeavySmemT<BIG_CFG>;
 static_assert(BF_WARP_MAX_SLOTS == 32, "warp tier: one slot per lane");
+// tuning-macro consistency (a violation would reach __trap or wrap a counter):
+// every distinct hashed key of a small-tier start fits its hash (distinct keys
+// <= w <= the tier's wedge cap); u8 counters hold d <= #slots; unit tables pack
+// chunk positions and lengths in 16 bits
+static_assert(512 >= BF_WARP_MAX_WEDGES, "warp hash (512 slots) must hold every key of a warp-tier start");
+static_assert(BF_MED_HS >= BF_MEDIUM_MAX_WEDGES, "medium hash must hold every key of a medium-tier start");
+static_assert(BF_MEDIUM_MAX_SLOTS <= 255 && BF_WARP_MAX_SLOTS <= 255, "u8 small-tier counters need d <= 255");
+static_assert(BF_BIG_CAP < 65536 && BF_MEDIUM_MAX_WEDGES < 65536 && SP_CAP < 65536,
+              "unit tables pack chunk positions in 16 bits");
 
 // ============================================================ output kernels
 // bv[side base + k] += sum over stripes of hub[stripe][side][k]
@@ -1133,6 +1141,21 @@ RowPool& row_pool(int dev) {
   static RowPool pools[64];
   return pools[dev & 63];
 }
+
+}  // namespace
+
+// the device's last graph is gone (bf_api.cu device_detach): give the rows back
+void row_pool_free(int dev) {
+  RowPool& pool = row_pool(dev);
+  std::lock_guard<std::mutex> lk(pool.m);
+  if (pool.p) cudaFree(pool.p);
+  if (pool.l) cudaFree(pool.l);
+  pool.p = pool.l = nullptr;
+  pool.bytes = pool.lbytes = 0;
+  pool.dirty = false;
+}
+
+namespace {
 
 template <int ORIENT, int MODE>
 void launch_tiers(bf_graph* g, CountArgs a, const uint32_t tier[4], uint32_t* queues, cudaStream_t s) {
@@ -1243,7 +1266,7 @@ bf_status graph_count(bf_graph* g, int mode, uint64_t* out_a, uint64_t* out_b, u
   }
   const uint32_t win = (g->opt.test_flags & BF_FLAG_SMALL_WINDOW) ? 64u : 0xFFFFFFFFu;
   const uint32_t cap = (g->opt.test_flags & BF_FLAG_SMALL_CHUNK) ? 64u : 0xFFFFFFFFu;
-  const uint64_t olen = std::max<uint64_t>(std::max(g->n_u, g->n_v), 1);
+  const uint64_t olen = std::max<uint64_t>(g->heavy_keys, 1);  // a heavy start's key offsets are < olen
   // the heavy tier's row pool is held for the whole call (rows must be clean
   // when the next call on this device starts)
   std::unique_lock<std::mutex> pool_lock;
@@ -1277,7 +1300,6 @@ bf_status graph_count(bf_graph* g, int mode, uint64_t* out_a, uint64_t* out_b, u
 #else
   a.exp = 0u;
 #endif
-  a.dbg_stop = getenv("BF_DBG_STOP") ? (uint32_t)atoi(getenv("BF_DBG_STOP")) : 0u;
   a.n_u = g->n_u;
   a.n_v = g->n_v;
   a.win = win;
@@ -1296,6 +1318,7 @@ bf_status graph_count(bf_graph* g, int mode, uint64_t* out_a, uint64_t* out_b, u
   }
 #endif
   CUDA_TRY(cudaEventRecord(g->ev[1], s));
+  NvtxRange nv_walk("bf a5-a7 wedge kernels");
   for (int r = first; r <= last; r++) {
     a.rank = r;
     a.world = G;
@@ -1357,8 +1380,10 @@ bf_status graph_count(bf_graph* g, int mode, uint64_t* out_a, uint64_t* out_b, u
     red_buf = dtot;
     red_cnt = 1;
   }
-  // a9: combine across GPUs
-  if (g->opt.world_size > 1) {
+  // a9: combine across GPUs (one in-place u64 allreduce over [counts | total];
+  // a 1-rank communicator runs the same path)
+  if (g->opt.nccl_comm) {
+    NvtxRange nv("bf a9 allreduce");
     bf_status st = nccl_allreduce_u64(g->opt.nccl_comm, red_buf, red_cnt, s);
     if (st != BF_OK) return st;
   }

@@ -6,6 +6,16 @@
 #include <string>
 #include <vector>
 #include "../../include/bf.h"
+#include <nvtx3/nvToolsExt.h>
+
+// NVTX range per phase (§8(a) rows) for nsys / ncu --nvtx; header-only, a
+// no-op unless a tool injects itself
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 #define BF_SMS_DEFAULT 148
 
@@ -44,11 +54,22 @@ struct bf_cuda_error {
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
-  cudaStream_t s = nullptr;  // stream-ordered allocation (device default pool)
+  cudaStream_t s = nullptr;  // stream-ordered allocation
+  cudaMemPool_t pool = nullptr;  // the library's private pool of the graph's device
   void ensure(size_t n);  // grow (no copy); throws bf_cuda_error
   void release();
   template <class T> T* as() const { return (T*)p; }
 };
+
+// ---- library-owned per-device state (bf_api.cu) --------------------------------
+// Every graph attaches to its device's library-owned caches: a private
+// stream-ordered memory pool (freed blocks stay cached, so repeated
+// create/destroy does not return to the driver; the device's default pool is
+// left alone) and the heavy tier's row pool (bf_count.cu).  Both persist
+// across graphs until bf_release_device_cache(device).
+cudaMemPool_t device_attach(int dev);  // throws bf_cuda_error
+void device_detach(int dev);
+void row_pool_free(int dev);  // bf_count.cu (takes the pool's lock)
 
 // ---- primitives (bf_prims.cu) -------------------------------------------------
 // Exclusive scan out[i] = Σ_{j<i} in[j]; *total (device, nullable) = Σ in.
@@ -105,6 +126,7 @@ struct bf_graph {
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   bool broken = false;  // after a CUDA/NCCL error
+  bool attached = false;  // holds a device_attach reference
   uint64_t launches = 0;
 
   uint32_t n_u = 0, n_v = 0;
@@ -139,6 +161,7 @@ struct bf_graph {
   // light (w <= t1)
   DevBuf order;         // u32 [n_tier sum]
   uint32_t n_tier[3] = {0, 0, 0};
+  uint64_t heavy_keys = 1;  // max key range of a heavy start (sizes the heavy rows)
   uint32_t t1 = 512, t2 = 2048;
 
   // split starts (a4): the first n_split heavy starts (w > split threshold)

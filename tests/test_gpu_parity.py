@@ -244,6 +244,7 @@ def test_repeated_graphs_same_process(bf, orient):
                 bu, bv_, t = bg.vertex()
                 assert t == ref["total"] and np.array_equal(bu, ref["b_u"]) and np.array_equal(bv_, ref["b_v"])
                 assert bg.total() == ref["total"], (rep, flags)
+        bf.bf_release_device_cache(0)  # rows and pool go back to the driver; the next graph reallocates
 
 
 @pytest.mark.parametrize("k,scale", [(1, 1.0), (2, 0.02), (3, 0.01), (4, 0.01), (5, 0.004)])
@@ -279,9 +280,10 @@ def test_sparsify_matches_oracle(bf, method, p):
         ref_kept = oracle.sparsify(g.n_u, g.edges, method, p, seed)
         assert np.array_equal(kept, ref_kept), (method, p, seed)
         ref = oracle.count(g.n_u, g.n_v, ref_kept, vertex=False, edge=False)["total"] if len(ref_kept) else 0
-        est = bf.approx_total(g.n_u, g.n_v, g.edges, p, method=method, seed=seed)
+        est, t_s, m_s = bf.bf_approx_total(g.n_u, g.n_v, g.edges, method, p, seed)
+        assert t_s == ref and m_s == len(ref_kept)
         scale = p ** -4 if method == "edge" else float(np.ceil(1.0 / p)) ** 3
-        assert est == ref * scale
+        assert est == pytest.approx(ref * scale, rel=1e-12)
     if p == 1.0:
         T = oracle.count(g.n_u, g.n_v, g.edges, vertex=False, edge=False)["total"]
         assert bf.approx_total(g.n_u, g.n_v, g.edges, 1.0, method=method) == T
@@ -332,3 +334,33 @@ def test_nccl_bootstrap_single_rank(bf):
     comm = bf.bf_nccl_comm_create(uid, 0, 1, 0)
     assert comm
     bf.bf_nccl_comm_destroy(comm)
+
+
+@pytest.mark.parametrize("V", [1, 3])
+def test_nccl_allreduce_combine(bf, V):
+    """a9 through the real ncclAllReduce: with a communicator attached (here a
+    1-rank one, the only kind one GPU can host) every count call combines its
+    [counts | total] buffer with ncclAllReduce(u64, sum) on the graph's stream;
+    with virtual ranks the on-device share sum feeds that same allreduce.  All
+    three modes stay bit-exact with the oracle."""
+    g = bfgen.config_graph(2, 0.01)
+    ref = oracle.count(g.n_u, g.n_v, g.edges)
+    comm = bf.bf_nccl_comm_create(bf.bf_nccl_unique_id(), 0, 1, 0)
+    try:
+        for orient in ORIENTS:
+            got = run_all(bf, g, "degree", orient, nccl_comm=comm, virtual_world=V)
+            assert_same(got, ref, f"nccl V={V} {orient}")
+    finally:
+        bf.bf_nccl_comm_destroy(comm)
+
+
+@pytest.mark.parametrize("k,scale", [(2, 0.02), (4, 0.01)])
+def test_rank_shares_partition(bf, k, scale):
+    """bf_rank_shares: the per-rank wedge loads of the kernels' deal partition W
+    exactly, for G = 1..8, and a virtual world of G ranks counts exactly."""
+    g = bfgen.config_graph(k, scale)
+    with bf.ButterflyGraph(g.n_u, g.n_v, g.edges, rank="degree") as bg:
+        W = bg.wedges()
+        for G in (1, 2, 3, 4, 8):
+            sh = bf.bf_rank_shares(bg.h, G)
+            assert len(sh) == G and sum(sh) == W, (G, sh, W)

@@ -1,7 +1,9 @@
 """N > 1 host path on CPU: world-size 2 and 3 process groups over gloo (127.0.0.1).
 
-Covers what the multi-GPU path does outside the kernels: broadcasting the
-128-byte NCCL id over the process group, the max-over-ranks timing reduction,
+Covers what the multi-GPU path does outside the kernels -- the same helpers
+bench.py's N > 1 branch calls (paper_1907_08607_b200/dist.py): the NCCL
+bootstrap (rank 0's 128-byte id broadcast over the process group, every rank
+joining with it), the max-over-ranks timing reduction,
 and the per-rank share of the wedge-sorted start lists (libbf's own deal
 function, bf_deal_index, which the kernels call): every start is processed by
 exactly one rank and the ranks' wedge loads are balanced.
@@ -32,9 +34,18 @@ def _worker(rank, world, port, q):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
+        from paper_1907_08607_b200 import bf
         from paper_1907_08607_b200 import dist as bfd
         payload = bytes((np.arange(128) * 7 + 3) % 256) if rank == 0 else None
         got = bfd.broadcast_bytes(payload)
+        # bench.py's bootstrap (dist.nccl_comm_for_group) with libbf's NCCL calls
+        # stubbed (no GPU here): rank 0 makes the id, every rank joins with it
+        made = []
+        bf.bf_nccl_unique_id = lambda: (made.append(1), bytes(range(128)))[1]
+        bf.bf_nccl_comm_create = lambda uid, r, w, d: ("comm", uid, r, w, d)
+        comm = bfd.nccl_comm_for_group(0)
+        assert comm == ("comm", bytes(range(128)), rank, world, 0)
+        assert len(made) == (1 if rank == 0 else 0)
         mx = bfd.max_over_ranks([rank * 1.5, 10.0 - rank])
         # a wedge-sorted list (descending) with a heavy head, cut into three tier segments
         rng = np.random.default_rng(0)

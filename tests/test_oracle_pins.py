@@ -327,3 +327,86 @@ def test_edge_order_invariance():
     key = lambda e: (e[:, 0].astype(np.int64) << 32) | e[:, 1]
     d = dict(zip(key(g.edges).tolist(), r["b_e"].tolist()))
     assert [d[k] for k in key(gp.edges).tolist()] == rp["b_e"].tolist()
+
+
+@pytest.mark.parametrize("procs", [1, 3, 7])
+def test_sharded_equals_unsharded(procs):
+    """the sharded oracle (forked workers over x ranges,
+    disjoint b(x)/b(e), centre partials summed) equals the single-process run
+    bit for bit, on either enumeration side, with ragged shard counts."""
+    g = bfgen.chung_lu(900, 700, 9000, 2.0, 2.3, seed=11)
+    with oracle.OracleGraph(g.n_u, g.n_v, g.edges) as og:
+        for side in (0, 1):
+            a = og.count(side=side)
+            b = og.count_sharded(procs=procs, side=side)
+            assert a["total"] == b["total"]
+            for k in ("b_u", "b_v", "b_e"):
+                assert np.array_equal(a[k], b[k]), (side, k)
+        e = bfgen.from_pairs(5, 3, [])
+        with oracle.OracleGraph(5, 3, e.edges) as og0:
+            r = og0.count_sharded(procs=procs)
+            assert r["total"] == 0 and not r["b_u"].any() and not r["b_v"].any() and len(r["b_e"]) == 0
+
+
+# ------------------------------------- approximate complement degeneracy ----
+def test_approx_codegen_hand_worked():
+    """Approximate complement degeneracy: rounds remove every
+    remaining vertex of the largest floor(log2 current degree).
+    Fig. 1: degrees u1 3, u2 3, u3 1, v1 2, v2 2, v3 3 -> buckets 1,1,0,1,1,1;
+    round 1 removes {u1,u2,v1,v2,v3} (gid order), leaving u3 at degree 0
+    (bucket -1): round 2.  Order u1,u2,v1,v2,v3,u3; W = 5 (x1=u1: v1->u2,
+    v2->u2, v3->u2, v3->u3; x1=u2: v3->u3).
+    A graph where the degree updates matter (U: h,x,y; V: p,q,a,b,c; edges
+    h-p,h-a,h-b,h-c,x-p,x-q,y-q): round 1 {h} (bucket 2); then p drops to
+    degree 1 but q keeps 2, so round 2 is {x,q} (bucket 1), not {x,p,q};
+    round 3 the rest at degree 0 in gid order: h,x,q,y,p,a,b,c."""
+    d, e = fig1()
+    with oracle.OracleGraph(3, 3, e) as og:
+        r = og.rank("approx_codegen")
+        assert r.tolist() == [0, 1, 5, 2, 3, 4]
+        assert og.wedges(r)[0] == 5
+    e2 = np.array([[0, 0], [0, 2], [0, 3], [0, 4], [1, 0], [1, 1], [2, 1]], np.uint32)
+    with oracle.OracleGraph(3, 5, e2) as og:
+        assert og.rank("approx_codegen").tolist() == [0, 1, 3, 4, 2, 5, 6, 7]
+
+
+@pytest.mark.parametrize("a,b", [(3, 9), (9, 3), (4, 5), (1, 6)])
+def test_approx_codegen_complete_bipartite(a, b):
+    """K_{a,b}: U vertices have degree b, V vertices degree a.  Different
+    log-buckets: the higher side goes in round 1 and the other side drops to
+    degree 0 (round 2) -- the side order with that side first.  Same bucket:
+    one round, gid order."""
+    g = bfgen.complete(a, b)
+    with oracle.OracleGraph(a, b, g.edges) as og:
+        r = og.rank("approx_codegen").tolist()
+    la, lb = (a).bit_length() - 1, (b).bit_length() - 1
+    if lb > la:
+        assert r == list(range(a + b))
+    elif la > lb:
+        assert r == list(range(b, a + b)) + list(range(b))
+    else:
+        assert r == list(range(a + b))
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_approx_codegen_work_bound(seed):
+    """The paper's work bound for this order: when x is peeled,
+    every remaining neighbour y has deg^r(y) <= 2 deg^r(x), hence for every edge
+    with rank(x) < rank(y): deg_x(y) = #{z in N(y): rank(z) > rank(x)} <= 2 deg(x).
+    The order is a permutation."""
+    g = bfgen.chung_lu(300 + 40 * seed, 200 + 30 * seed, 3000 + 500 * seed, 2.0, 2.3, seed=seed)
+    n = g.n_u + g.n_v
+    with oracle.OracleGraph(g.n_u, g.n_v, g.edges) as og:
+        r = og.rank("approx_codegen").astype(np.int64)
+    assert sorted(r.tolist()) == list(range(n))
+    gu = g.edges[:, 0].astype(np.int64)
+    gv = g.n_u + g.edges[:, 1].astype(np.int64)
+    deg = np.bincount(np.concatenate([gu, gv]), minlength=n)
+    nbrs = [[] for _ in range(n)]
+    for u, v in zip(gu.tolist(), gv.tolist()):
+        nbrs[u].append(v)
+        nbrs[v].append(u)
+    for x, y in list(zip(gu.tolist(), gv.tolist())) + list(zip(gv.tolist(), gu.tolist())):
+        if r[x] < r[y]:
+            degxy = sum(1 for z in nbrs[y] if r[z] > r[x])
+            assert degxy <= 2 * deg[x], (x, y)
