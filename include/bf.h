@@ -55,13 +55,28 @@ typedef enum {
  *  BF_RANK_APPROX_DEGREE decreasing floor(log2 deg), deg 0 last (reading Z3),
  *                        ties by global id gid = u | n_u + v (reading Z2).
  *  BF_RANK_DEGREE        decreasing degree, ties by gid (reading Z2).
+ *  BF_RANK_APPROX_CODEGEN approximate complement degeneracy (P:413-426,
+ *                        work-efficient by P:1569-1581): rounds of a parallel
+ *                        peel, each removing every remaining vertex whose
+ *                        floor(log2 of its degree among the remaining vertices)
+ *                        is the current maximum (deg 0 -> -1), at most 33
+ *                        rounds; earlier rounds rank first, ties by gid
+ *                        (readings Z2, Z16).
  *  BF_RANK_AUTO          the paper's runtime choice: with w_s the
- *                        wedges under side order and w_r the fewer of degree /
- *                        approximate-degree order (both computed in O(m) before
- *                        ranking, W = Σ_y (k_y d_y − k_y(k_y+1)/2)), side order
- *                        if f = (w_s − w_r)/w_s < 0.1, else that other order.
+ *                        wedges under side order and w_r the fewest of degree /
+ *                        approximate-degree / approximate complement degeneracy
+ *                        order (computed before ranking, W = Σ_y (k_y d_y −
+ *                        k_y(k_y+1)/2)), side order if f = (w_s − w_r)/w_s <
+ *                        0.1, else that other order (ties: degree, approximate
+ *                        degree, approximate complement degeneracy).
  *                        bf_rank_info reports the choice.                      */
-typedef enum { BF_RANK_SIDE = 0, BF_RANK_APPROX_DEGREE = 1, BF_RANK_DEGREE = 2, BF_RANK_AUTO = 3 } bf_rank_kind;
+typedef enum {
+  BF_RANK_SIDE = 0,
+  BF_RANK_APPROX_DEGREE = 1,
+  BF_RANK_DEGREE = 2,
+  BF_RANK_AUTO = 3,
+  BF_RANK_APPROX_CODEGEN = 4
+} bf_rank_kind;
 
 /* Wedge retrieval orientation.  Both retrieve exactly the same wedge set
  * {(x1,y,x2): rank(y) > rank(x1), rank(x2) > rank(x1)} (Fig.
@@ -152,10 +167,11 @@ bf_status bf_count_edge(bf_graph* g, uint64_t* out_e, uint64_t* total);
 bf_status bf_wedge_count(const bf_graph* g, uint64_t* w);
 
 /* The ranking in effect after bf_rank (*kind: BF_RANK_SIDE / APPROX_DEGREE /
- * DEGREE; BF_RANK_AUTO resolved) and, after BF_RANK_AUTO only, the wedges each
- * candidate processes (w[0] side, w[1] approximate degree, w[2] degree; zeros
+ * DEGREE / APPROX_CODEGEN; BF_RANK_AUTO resolved) and, after BF_RANK_AUTO
+ * only, the wedges each candidate processes (w[0] side, w[1] approximate
+ * degree, w[2] degree, w[3] approximate complement degeneracy; zeros
  * otherwise).  Either pointer may be NULL.  Errors: BF_EINVAL, BF_ENORANK. */
-bf_status bf_rank_info(const bf_graph* g, int* kind, uint64_t w[3]);
+bf_status bf_rank_info(const bf_graph* g, int* kind, uint64_t w[4]);
 
 /* Statistics of the last bf_count_* call (host outputs, each nullable):
  * kernel_ms = CUDA-event time of its wedge kernel(s) alone, call_ms = of the

@@ -24,9 +24,9 @@ if not os.path.exists(LIB_PATH):
 _lib = ctypes.CDLL(LIB_PATH)
 
 BF_OK, BF_EINVAL, BF_ERANGE, BF_EDUP, BF_ENOMEM, BF_ECUDA, BF_ENCCL, BF_ENORANK, BF_EOVERFLOW = range(9)
-BF_RANK_SIDE, BF_RANK_APPROX_DEGREE, BF_RANK_DEGREE, BF_RANK_AUTO = 0, 1, 2, 3
+BF_RANK_SIDE, BF_RANK_APPROX_DEGREE, BF_RANK_DEGREE, BF_RANK_AUTO, BF_RANK_APPROX_CODEGEN = 0, 1, 2, 3, 4
 RANK_KINDS = {"side": BF_RANK_SIDE, "approx_degree": BF_RANK_APPROX_DEGREE, "degree": BF_RANK_DEGREE,
-              "auto": BF_RANK_AUTO}
+              "auto": BF_RANK_AUTO, "approx_codegen": BF_RANK_APPROX_CODEGEN}
 RANK_NAMES = {v: k for k, v in RANK_KINDS.items()}
 BF_ORIENT_AUTO, BF_ORIENT_LOW, BF_ORIENT_HIGH = 0, 1, 2
 ORIENTS = {"auto": BF_ORIENT_AUTO, "low": BF_ORIENT_LOW, "high": BF_ORIENT_HIGH}
@@ -152,9 +152,10 @@ def bf_wedge_count(g) -> int:
 
 
 def bf_rank_info(g):
-    """(ranking in effect, [w_side, w_approx_degree, w_degree]) -- the w's only after BF_RANK_AUTO."""
+    """(ranking in effect, [w_side, w_approx_degree, w_degree, w_approx_codegen]) -- the w's only
+    after BF_RANK_AUTO."""
     k = ctypes.c_int(0)
-    w = (ctypes.c_uint64 * 3)()
+    w = (ctypes.c_uint64 * 4)()
     _check(_lib.bf_rank_info(g, ctypes.byref(k), w), "bf_rank_info")
     return RANK_NAMES[k.value], [int(x) for x in w]
 

@@ -190,7 +190,7 @@ bf_status bf_graph_create(uint32_t n_u, uint32_t n_v, const uint32_t* edges, uin
 bf_status bf_rank(bf_graph* g, bf_rank_kind kind) {
   if (!g) { bf_set_error("g is NULL"); return BF_EINVAL; }
   if (g->broken) { bf_set_error("graph unusable after a CUDA/NCCL error"); return BF_ECUDA; }
-  if (kind < BF_RANK_SIDE || kind > BF_RANK_AUTO) { bf_set_error("bad rank kind"); return BF_EINVAL; }
+  if (kind < BF_RANK_SIDE || kind > BF_RANK_APPROX_CODEGEN) { bf_set_error("bad rank kind"); return BF_EINVAL; }
   DeviceGuard dg(g->device);
   g->ranked = false;
   bf_status st = guarded(g, [&]() -> bf_status {
@@ -207,12 +207,12 @@ bf_status bf_rank(bf_graph* g, bf_rank_kind kind) {
   return st;
 }
 
-bf_status bf_rank_info(const bf_graph* g, int* kind, uint64_t w[3]) {
+bf_status bf_rank_info(const bf_graph* g, int* kind, uint64_t w[4]) {
   if (!g) { bf_set_error("g is NULL"); return BF_EINVAL; }
   if (!g->ranked) { bf_set_error("bf_rank has not been called"); return BF_ENORANK; }
   if (kind) *kind = g->rank_kind;
   if (w)
-    for (int i = 0; i < 3; i++) w[i] = g->w_auto[i];
+    for (int i = 0; i < 4; i++) w[i] = g->w_auto[i];
   return BF_OK;
 }
 

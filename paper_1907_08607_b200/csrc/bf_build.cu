@@ -76,7 +76,8 @@ __global__ void k_side_sums(const uint32_t* __restrict__ deg, uint64_t n, uint32
 // a side (degree: dmax - d; approximate degree: 63 - floor(log2 d) or 64; side
 // order: none), so the vertex sort runs over tb + 1 bits only
 __global__ void k_rank_keys(const uint32_t* __restrict__ deg, uint64_t n, uint32_t nU, int kind, int tb,
-                            uint32_t dmax, const unsigned long long* __restrict__ sums, uint32_t* __restrict__ skey,
+                            uint32_t dmax, const unsigned long long* __restrict__ sums,
+                            const uint8_t* __restrict__ peel, uint32_t* __restrict__ skey,
                             uint32_t* __restrict__ iota, uint64_t* __restrict__ rkey_gid) {
   int u_first = kind == BF_RANK_SIDE ? (sums[0] <= sums[1]) : 1;
   for (uint64_t z = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; z < n; z += (uint64_t)gridDim.x * blockDim.x) {
@@ -85,6 +86,7 @@ __global__ void k_rank_keys(const uint32_t* __restrict__ deg, uint64_t n, uint32
     uint32_t tier;
     if (kind == BF_RANK_DEGREE) tier = 0x7FFFFFFFu - d;                           // decreasing degree
     else if (kind == BF_RANK_APPROX_DEGREE) tier = d ? 63u - (31u - __clz(d)) : 64u;  // decreasing floor(log2 d)
+    else if (kind == BF_RANK_APPROX_CODEGEN) tier = peel[z];                      // peel round
     else tier = (side == 0) == (u_first != 0) ? 0u : 1u;                          // first side, then the other
     const uint32_t tc = kind == BF_RANK_SIDE ? 0u : kind == BF_RANK_DEGREE ? dmax - d : tier;
     skey[z] = (side << tb) | tc;
@@ -104,6 +106,64 @@ __global__ void k_rid_maps(const uint32_t* __restrict__ gid_of_rid, uint64_t n, 
   }
 }
 
+// ---- a2: approximate complement degeneracy --------
+// Rounds of a parallel peel: round r removes every remaining vertex whose
+// floor(log2 of its degree among the remaining vertices) is the current
+// maximum (reading Z16), then lowers its remaining neighbours' degrees.  The
+// maximum bucket strictly decreases from round to round (all vertices of it
+// leave; degrees only fall), so there are at most 33 rounds (buckets 31..0 and
+// deg 0).  code = floor(log2 d) + 2 in [1, 33] (d = 0 -> 1); 0 = no vertex left.
+constexpr uint8_t PEEL_ALIVE = 0xFF;
+constexpr int PEEL_ROUNDS = 33;
+__device__ __forceinline__ uint32_t peel_code(uint32_t d) { return d ? 33u - __clz(d) : 1u; }
+
+__global__ void k_peel_max(const uint32_t* __restrict__ cur, const uint8_t* __restrict__ rnd, uint64_t n,
+                           uint32_t* __restrict__ code) {
+  uint32_t best = 0;
+  for (uint64_t z = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; z < n; z += (uint64_t)gridDim.x * blockDim.x)
+    if (rnd[z] == PEEL_ALIVE) best = max(best, peel_code(cur[z]));
+  best = __reduce_max_sync(0xffffffffu, best);
+  if ((threadIdx.x & 31) == 0 && best) atomicMax(code, best);
+}
+
+__global__ void k_peel_mark(const uint32_t* __restrict__ cur, uint8_t* __restrict__ rnd, uint64_t n,
+                            const uint32_t* __restrict__ code, int r) {
+  const uint32_t c = *code;
+  if (!c) return;
+  for (uint64_t z = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; z < n; z += (uint64_t)gridDim.x * blockDim.x)
+    if (rnd[z] == PEEL_ALIVE && peel_code(cur[z]) == c) rnd[z] = (uint8_t)r;
+}
+
+// remaining neighbours of this round's vertices lose one degree per edge
+// (warp-aggregated: a round often removes many neighbours of one hub)
+__device__ __forceinline__ void sub_degree(uint32_t* cur, uint32_t z, bool valid) {
+  const uint32_t act = __ballot_sync(0xffffffffu, valid);
+  if (!valid) return;
+  const uint32_t peers = __match_any_sync(act, z);
+  if ((threadIdx.x & 31) == (uint32_t)(__ffs(peers) - 1)) atomicSub(&cur[z], (uint32_t)__popc(peers));
+}
+
+__global__ void k_peel_edges(const uint32_t* __restrict__ e, uint64_t m, uint32_t nU, uint32_t* __restrict__ cur,
+                             const uint8_t* __restrict__ rnd, const uint32_t* __restrict__ code, int r) {
+  if (!*code) return;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i0 = blockIdx.x * (uint64_t)blockDim.x + (threadIdx.x & ~31u); i0 < m; i0 += stride) {
+    const uint64_t i = i0 + (threadIdx.x & 31);
+    uint32_t gu = 0, gv = 0;
+    bool du = false, dv = false;
+    if (i < m) {
+      const uint2 uv = reinterpret_cast<const uint2*>(e)[i];
+      gu = uv.x;
+      gv = nU + uv.y;
+      const uint8_t ru = rnd[gu], rv = rnd[gv];
+      du = ru == (uint8_t)r && rv == PEEL_ALIVE;  // u leaves now, v stays: v loses one
+      dv = rv == (uint8_t)r && ru == PEEL_ALIVE;
+    }
+    sub_degree(cur, gv, du);
+    sub_degree(cur, gu, dv);
+  }
+}
+
 // ---- a2 (auto): the paper's f metric ---------------------------
 // W under degree and approximate-degree order without ranking the graph: with
 // k_y = #neighbours of y ranked before y, W = sum_y (k_y d_y - k_y (k_y+1)/2)
@@ -114,34 +174,43 @@ __device__ __forceinline__ uint64_t rank_key(uint32_t d, uint64_t gid, int appro
   return ((uint64_t)tier << 32) | gid;
 }
 
-__global__ void k_auto_k(const uint32_t* __restrict__ e, uint64_t m, uint32_t nU, const uint32_t* __restrict__ deg,
-                         uint32_t* __restrict__ k_deg, uint32_t* __restrict__ k_adeg) {
+// k_y per candidate order c (0 degree, 1 approximate degree, 2 approximate
+// complement degeneracy): k[c*n + y] = #neighbours ranked before y
+__global__ void k_auto_k(const uint32_t* __restrict__ e, uint64_t m, uint32_t nU, uint64_t n,
+                         const uint32_t* __restrict__ deg, const uint8_t* __restrict__ peel, uint32_t* __restrict__ k) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
     const uint2 uv = reinterpret_cast<const uint2*>(e)[i];
     const uint64_t gu = uv.x, gv = (uint64_t)nU + uv.y;
     const uint32_t du = deg[gu], dv = deg[gv];
     // the endpoint ranked first is the neighbour "ranked before" the other (its centre)
-    atomicAdd(&k_deg[rank_key(du, gu, 0) < rank_key(dv, gv, 0) ? gv : gu], 1u);
-    atomicAdd(&k_adeg[rank_key(du, gu, 1) < rank_key(dv, gv, 1) ? gv : gu], 1u);
+    atomicAdd(&k[rank_key(du, gu, 0) < rank_key(dv, gv, 0) ? gv : gu], 1u);
+    atomicAdd(&k[n + (rank_key(du, gu, 1) < rank_key(dv, gv, 1) ? gv : gu)], 1u);
+    const uint64_t cu = ((uint64_t)peel[gu] << 32) | gu, cv = ((uint64_t)peel[gv] << 32) | gv;
+    atomicAdd(&k[2 * n + (cu < cv ? gv : gu)], 1u);
   }
 }
 
-__global__ void k_auto_w(const uint32_t* __restrict__ deg, const uint32_t* __restrict__ k_deg,
-                         const uint32_t* __restrict__ k_adeg, uint64_t n, unsigned long long* __restrict__ w) {
-  __shared__ unsigned long long s[2];
-  if (threadIdx.x < 2) s[threadIdx.x] = 0;
+__global__ void k_auto_w(const uint32_t* __restrict__ deg, const uint32_t* __restrict__ k, uint64_t n,
+                         unsigned long long* __restrict__ w) {
+  __shared__ unsigned long long s[3];
+  if (threadIdx.x < 3) s[threadIdx.x] = 0;
   __syncthreads();
-  unsigned long long a = 0, b = 0;
+  unsigned long long acc[3] = {0, 0, 0};
   for (uint64_t z = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; z < n; z += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t d = deg[z], k1 = k_deg[z], k2 = k_adeg[z];
-    a += k1 * d - k1 * (k1 + 1) / 2;
-    b += k2 * d - k2 * (k2 + 1) / 2;
+    const uint64_t d = deg[z];
+#pragma unroll
+    for (int c = 0; c < 3; c++) {
+      const uint64_t kk = k[c * n + z];
+      acc[c] += kk * d - kk * (kk + 1) / 2;
+    }
   }
-  a = warp_sum(a);
-  b = warp_sum(b);
-  if ((threadIdx.x & 31) == 0) { atomicAdd(&s[0], a); atomicAdd(&s[1], b); }
+#pragma unroll
+  for (int c = 0; c < 3; c++) {
+    acc[c] = warp_sum(acc[c]);
+    if ((threadIdx.x & 31) == 0) atomicAdd(&s[c], acc[c]);
+  }
   __syncthreads();
-  if (threadIdx.x < 2) atomicAdd(&w[threadIdx.x], s[threadIdx.x]);
+  if (threadIdx.x < 3) atomicAdd(&w[threadIdx.x], s[threadIdx.x]);
 }
 
 // ---- a3 -----------------------------------------------------------------------
@@ -358,55 +427,87 @@ bf_status graph_ingest(bf_graph* g, const uint32_t* edges) {
   return BF_OK;
 }
 
+// approximate complement degeneracy: g->peel[gid] = removal round (a2)
+static void peel_rounds(bf_graph* g) {
+  cudaStream_t s = g->stream;
+  const uint64_t n = g->n, m = g->m, n1 = std::max<uint64_t>(n, 1);
+  g->peel.ensure(n1 + 64);
+  g->tmp_f.ensure(n1 * 4 + 64);
+  g->tmp_b.ensure(256);
+  uint32_t* cur = g->tmp_f.as<uint32_t>();
+  uint32_t* code = (uint32_t*)(g->tmp_b.as<char>() + 96);  // [PEEL_ROUNDS]
+  uint8_t* rnd = g->peel.as<uint8_t>();
+  CUDA_TRY(cudaMemsetAsync(rnd, PEEL_ALIVE, n1, s));
+  CUDA_TRY(cudaMemsetAsync(code, 0, PEEL_ROUNDS * 4, s));
+  if (n) CUDA_TRY(cudaMemcpyAsync(cur, g->deg.p, n * 4, cudaMemcpyDeviceToDevice, s));
+  // no host sync: a round with no vertex left (code 0) returns at once
+  for (int r = 0; r < PEEL_ROUNDS && n; r++) {
+    k_peel_max<<<grid_for(n, g->sms), TPB, 0, s>>>(cur, rnd, n, code + r);
+    KERNEL_CHECK(g);
+    k_peel_mark<<<grid_for(n, g->sms), TPB, 0, s>>>(cur, rnd, n, code + r, r);
+    KERNEL_CHECK(g);
+    if (m) {
+      k_peel_edges<<<grid_for(m, g->sms), TPB, 0, s>>>(g->edges.as<uint32_t>(), m, g->n_u, cur, rnd, code + r, r);
+      KERNEL_CHECK(g);
+    }
+  }
+  g->peel_valid = true;
+}
+
 // BF_RANK_AUTO: side order if f = (w_s - w_r) / w_s < 0.1, else the one of
-// degree / approximate-degree order with fewer wedges
+// degree / approximate-degree / approximate complement degeneracy order with
+// the fewest wedges
 static bf_status rank_auto(bf_graph* g, int* kind) {
   cudaStream_t s = g->stream;
   const uint64_t n = g->n, m = g->m, n1 = std::max<uint64_t>(n, 1);
-  g->tmp_c.ensure(n1 * 4 + 64);
-  g->tmp_d.ensure(n1 * 4 + 64);
-  g->tmp_b.ensure(64);
-  uint32_t* kd = g->tmp_c.as<uint32_t>();
-  uint32_t* ka = g->tmp_d.as<uint32_t>();
-  unsigned long long* w = g->tmp_b.as<unsigned long long>();  // [0] degree, [1] approx, [2..3] side sums
-  CUDA_TRY(cudaMemsetAsync(kd, 0, n1 * 4, s));
-  CUDA_TRY(cudaMemsetAsync(ka, 0, n1 * 4, s));
-  CUDA_TRY(cudaMemsetAsync(w, 0, 32, s));
+  peel_rounds(g);
+  g->tmp_c.ensure(n1 * 12 + 64);
+  g->tmp_b.ensure(256);
+  uint32_t* k = g->tmp_c.as<uint32_t>();
+  unsigned long long* w = g->tmp_b.as<unsigned long long>();  // [0] degree, [1] approx, [2] codegen, [3..4] side sums
+  CUDA_TRY(cudaMemsetAsync(k, 0, n1 * 12, s));
+  CUDA_TRY(cudaMemsetAsync(w, 0, 40, s));
   if (n) {
-    k_side_sums<<<grid_for(n, g->sms), TPB, 0, s>>>(g->deg.as<uint32_t>(), n, g->n_u, w + 2);
+    k_side_sums<<<grid_for(n, g->sms), TPB, 0, s>>>(g->deg.as<uint32_t>(), n, g->n_u, w + 3);
     KERNEL_CHECK(g);
   }
   if (m) {
-    k_auto_k<<<grid_for(m, g->sms), TPB, 0, s>>>(g->edges.as<uint32_t>(), m, g->n_u, g->deg.as<uint32_t>(), kd, ka);
+    k_auto_k<<<grid_for(m, g->sms), TPB, 0, s>>>(g->edges.as<uint32_t>(), m, g->n_u, n, g->deg.as<uint32_t>(),
+                                                  g->peel.as<uint8_t>(), k);
     KERNEL_CHECK(g);
   }
   if (n) {
-    k_auto_w<<<grid_for(n, g->sms), TPB, 0, s>>>(g->deg.as<uint32_t>(), kd, ka, n, w);
+    k_auto_w<<<grid_for(n, g->sms), TPB, 0, s>>>(g->deg.as<uint32_t>(), k, n, w);
     KERNEL_CHECK(g);
   }
-  unsigned long long h[4];
-  CUDA_TRY(cudaMemcpyAsync(h, w, 32, cudaMemcpyDeviceToHost, s));
+  unsigned long long h[5];
+  CUDA_TRY(cudaMemcpyAsync(h, w, 40, cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaStreamSynchronize(s));
-  const uint64_t w_side = std::min<uint64_t>(h[2], h[3]);  // reading Z1: the cheaper side as endpoints
-  const uint64_t w_deg = h[0], w_adeg = h[1];
-  const uint64_t w_r = std::min(w_deg, w_adeg);
+  const uint64_t w_side = std::min<uint64_t>(h[3], h[4]);  // reading Z1: the cheaper side as endpoints
+  const uint64_t w_deg = h[0], w_adeg = h[1], w_cg = h[2];
+  const uint64_t w_r = std::min(std::min(w_deg, w_adeg), w_cg);
   g->w_auto[0] = w_side;
   g->w_auto[1] = w_adeg;
   g->w_auto[2] = w_deg;
+  g->w_auto[3] = w_cg;
   // f < 0.1  <=>  10 (w_s - w_r) < w_s (integer arithmetic; f <= 0 when w_r >= w_s)
   const bool side = w_r >= w_side || (unsigned __int128)10 * (w_side - w_r) < (unsigned __int128)w_side;
-  *kind = side ? BF_RANK_SIDE : (w_deg <= w_adeg ? BF_RANK_DEGREE : BF_RANK_APPROX_DEGREE);
+  // ties between the other three: degree, then approximate degree, then approximate complement degeneracy
+  *kind = side ? BF_RANK_SIDE
+               : (w_deg == w_r ? BF_RANK_DEGREE : (w_adeg == w_r ? BF_RANK_APPROX_DEGREE : BF_RANK_APPROX_CODEGEN));
   return BF_OK;
 }
 
 bf_status graph_rank(bf_graph* g, int kind) {
   cudaStream_t s = g->stream;
+  g->peel_valid = false;
   if (kind == BF_RANK_AUTO) {
     bf_status st = rank_auto(g, &kind);
     if (st != BF_OK) return st;
   } else {
-    g->w_auto[0] = g->w_auto[1] = g->w_auto[2] = 0;
+    for (auto& x : g->w_auto) x = 0;
   }
+  if (kind == BF_RANK_APPROX_CODEGEN && !g->peel_valid) peel_rounds(g);
   const uint64_t n = g->n, m = g->m, S = 2 * m;
   const uint64_t n1 = std::max<uint64_t>(n, 1), S1 = std::max<uint64_t>(S, 1);
   g->rid_of_gid.ensure(n1 * 4);
@@ -444,11 +545,12 @@ bf_status graph_rank(bf_graph* g, int kind) {
   }
   // a vertex's degree is at most the other side's size
   uint32_t dmax = std::max(g->n_u, g->n_v);
-  int tb = kind == BF_RANK_SIDE ? 0 : kind == BF_RANK_APPROX_DEGREE ? 7 : ceil_log2_u64((uint64_t)dmax + 1);
+  int tb = kind == BF_RANK_SIDE ? 0 : kind == BF_RANK_APPROX_DEGREE ? 7
+           : kind == BF_RANK_APPROX_CODEGEN ? 6 : ceil_log2_u64((uint64_t)dmax + 1);
   if (tb > 31) { tb = 31; dmax = 0x7FFFFFFFu; }  // degrees stay below 2^31 (m < 2^31 per vertex)
   if (n) {
-    k_rank_keys<<<grid_for(n, g->sms), TPB, 0, s>>>(g->deg.as<uint32_t>(), n, g->n_u, kind, tb, dmax, sums, skey0,
-                                                     val0, rkey_gid);
+    k_rank_keys<<<grid_for(n, g->sms), TPB, 0, s>>>(g->deg.as<uint32_t>(), n, g->n_u, kind, tb, dmax, sums,
+                                                     g->peel.as<uint8_t>(), skey0, val0, rkey_gid);
     KERNEL_CHECK(g);
   }
   int which = radix_sort_u32(skey0, val0, skey1, val1, n, 0, tb + 1, tmp, s, L);

@@ -139,7 +139,9 @@ struct bf_graph {
   // a2/a3: ranking and ranked CSR (rid space)
   bool ranked = false;
   int rank_kind = -1;       // the ranking in effect (BF_RANK_AUTO resolves to one of the others)
-  uint64_t w_auto[3] = {0, 0, 0};  // BF_RANK_AUTO: W under side, approximate-degree, degree order
+  uint64_t w_auto[4] = {0, 0, 0, 0};  // BF_RANK_AUTO: W under side, approx.-degree, degree, approx. codegen order
+  DevBuf peel;                // u8 [n] removal round of approximate complement degeneracy (gid order)
+  bool peel_valid = false;
   int orient = BF_ORIENT_HIGH;
   DevBuf rid_of_gid;  // u32 [n]
   DevBuf gid_of_rid;  // u32 [n]
@@ -202,7 +204,7 @@ struct bf_graph {
 
   template <class F> void for_each_buf(F f) {
     DevBuf* bufs[] = {&edges, &deg, &rid_of_gid, &gid_of_rid, &rkey, &off, &nbr, &pos, &hi, &where,
-                      &wstart, &seglo, &seglen, &wpre, &items, &order, &bv, &acc, &be, &total, &orow, &otouch, &queue, &hub, &dflag, &split, &split_off, &split_cnt, &pieces, &srow, &slist,
+                      &wstart, &peel, &seglo, &seglen, &wpre, &items, &order, &bv, &acc, &be, &total, &orow, &otouch, &queue, &hub, &dflag, &split, &split_off, &split_cnt, &pieces, &srow, &slist,
                       &tmp_a, &tmp_b, &tmp_c, &tmp_d, &tmp_e, &tmp_f, &tmp_scan};
     for (DevBuf* b : bufs) f(*b);
   }

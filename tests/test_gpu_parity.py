@@ -19,7 +19,7 @@ import oracle
 pytestmark = pytest.mark.gpu
 
 GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
-RANKS = ("side", "approx_degree", "degree")
+RANKS = ("side", "approx_degree", "degree", "approx_codegen")
 ORIENTS = ("high", "low")
 
 
@@ -249,23 +249,45 @@ def test_repeated_graphs_same_process(bf, orient):
 
 @pytest.mark.parametrize("k,scale", [(1, 1.0), (2, 0.02), (3, 0.01), (4, 0.01), (5, 0.004)])
 def test_rank_auto_f_metric(bf, k, scale):
-    """BF_RANK_AUTO: the wedge counts of the three candidate orders
+    """BF_RANK_AUTO: the wedge counts of the four candidate orders
     computed before ranking equal the oracle's W for each order; the choice
-    follows f = (w_s - w_r)/w_s < 0.1 -> side; the counts stay exact."""
+    follows f = (w_s - w_r)/w_s < 0.1 -> side, else the cheapest other order;
+    the counts stay exact."""
     g = bfgen.config_graph(k, scale)
+    kinds = ("side", "approx_degree", "degree", "approx_codegen")
     with oracle.OracleGraph(g.n_u, g.n_v, g.edges) as og:
-        W = {kind: og.wedges(og.rank(kind))[0] for kind in ("side", "approx_degree", "degree")}
+        W = {kind: og.wedges(og.rank(kind))[0] for kind in kinds}
     ref = oracle.count(g.n_u, g.n_v, g.edges, edge=False)
     with bf.ButterflyGraph(g.n_u, g.n_v, g.edges, rank="auto") as bg:
         kind, w = bg.rank_info()
-        assert w == [W["side"], W["approx_degree"], W["degree"]]
-        wr = min(W["degree"], W["approx_degree"])
+        assert w == [W[x] for x in kinds]
+        wr = min(W["degree"], W["approx_degree"], W["approx_codegen"])
         side = wr >= W["side"] or 10 * (W["side"] - wr) < W["side"]
-        expect = "side" if side else ("degree" if W["degree"] <= W["approx_degree"] else "approx_degree")
+        expect = "side" if side else next(x for x in ("degree", "approx_degree", "approx_codegen") if W[x] == wr)
         assert kind == expect
         assert bg.wedges() == W[kind]
         bu, bv, t = bg.vertex()
         assert t == ref["total"] and np.array_equal(bu, ref["b_u"]) and np.array_equal(bv, ref["b_v"])
+
+
+@pytest.mark.parametrize("k,scale", [(1, 1.0), (2, 0.02), (3, 0.01), (4, 0.01), (5, 0.004)])
+def test_rank_approx_codegen(bf, k, scale):
+    """Approximate complement degeneracy on the GPU (bucketed peel, <= 33
+    rounds): the rank order inside each side equals the oracle's order, W equals
+    the oracle's W under it, and every output is exact."""
+    g = bfgen.config_graph(k, scale)
+    n = g.n_u + g.n_v
+    ref = oracle.count(g.n_u, g.n_v, g.edges)
+    with oracle.OracleGraph(g.n_u, g.n_v, g.edges) as og:
+        rref = og.rank("approx_codegen")
+        W_ref = og.wedges(rref)[0]
+    for orient in ORIENTS:
+        with bf.ButterflyGraph(g.n_u, g.n_v, g.edges, rank="approx_codegen", orient=orient) as bg:
+            assert bg.wedges() == W_ref
+            rid = bg.export_csr()["rid_of_gid"].astype(np.int64)
+        for lo, hi in ((0, g.n_u), (g.n_u, n)):
+            assert (np.argsort(rid[lo:hi]) == np.argsort(rref[lo:hi])).all()
+        assert_same(run_all(bf, g, "approx_codegen", orient), ref, f"c{k} approx_codegen/{orient}")
 
 
 @pytest.mark.parametrize("method", ["edge", "color"])
@@ -317,7 +339,7 @@ def test_random_graphs_random_paths(bf, seed):
     for nm in names:
         if rng.random() < 0.3:
             f |= getattr(bf, "BF_FLAG_" + nm)
-    rank = ["side", "approx_degree", "degree", "auto"][int(rng.integers(0, 4))]
+    rank = ["side", "approx_degree", "degree", "auto", "approx_codegen"][int(rng.integers(0, 5))]
     orient = ORIENTS[int(rng.integers(0, 2))]
     opts = dict(test_flags=f)
     if rng.random() < 0.3:
