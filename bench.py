@@ -89,6 +89,11 @@ class ClockSampler:
     def timed(self, t0: float, t1: float):
         self.windows.append((t0, t1))
 
+    def wait_first(self, limit: float = 5.0):
+        t = time.time()
+        while self.proc and not self.lines and time.time() - t < limit:
+            time.sleep(0.02)
+
     def __exit__(self, *a):
         if self.proc:
             self.proc.terminate()
@@ -365,7 +370,7 @@ def main():
     times, kms, cms, launches, pairs = [], [], [], 0, []
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(dev.index) as clk:
-        time.sleep(0.3)  # nvidia-smi is up and sampling
+        clk.wait_first()  # nvidia-smi is up and sampling
         for _ in range(a.steps):
             flush.fill_(1)  # L2 flush between timed steps (256 MiB > 126 MB L2)
             torch.cuda.synchronize(dev)

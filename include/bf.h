@@ -109,6 +109,12 @@ typedef enum { BF_ORIENT_AUTO = 0, BF_ORIENT_LOW = 1, BF_ORIENT_HIGH = 2 } bf_or
 #define BF_FLAG_UNPACKED_SORT   0x80u /* bf_rank: slot sort with separate key and value
                                          arrays (the path taken when rank bits + edge-id
                                          bits exceed 64)                                */
+#define BF_FLAG_NO_DENSE_ROW    0x100u /* never count split pieces in a whole-key-range
+                                         shared row (taken when every heavy start has at
+                                         most 40960 same-side keys, e.g. config 4)       */
+#define BF_FLAG_KEY_BUFFER      0x200u /* vertex mode: slot-mode walks always keep their
+                                         keys for pass 2 (taken when the average
+                                         segment is short, e.g. config 4)                */
 
 typedef struct {
   int device;               /* CUDA ordinal                                           */

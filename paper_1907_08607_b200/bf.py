@@ -31,7 +31,8 @@ RANK_NAMES = {v: k for k, v in RANK_KINDS.items()}
 BF_ORIENT_AUTO, BF_ORIENT_LOW, BF_ORIENT_HIGH = 0, 1, 2
 ORIENTS = {"auto": BF_ORIENT_AUTO, "low": BF_ORIENT_LOW, "high": BF_ORIENT_HIGH}
 BF_FLAG_FORCE_WARP, BF_FLAG_FORCE_CTA, BF_FLAG_SMALL_WINDOW, BF_FLAG_FORCE_DENSE = 0x1, 0x2, 0x4, 0x10
-BF_FLAG_SMALL_CHUNK, BF_FLAG_NO_SPLIT, BF_FLAG_UNPACKED_SORT = 0x20, 0x40, 0x80
+BF_FLAG_SMALL_CHUNK, BF_FLAG_NO_SPLIT, BF_FLAG_UNPACKED_SORT, BF_FLAG_NO_DENSE_ROW = 0x20, 0x40, 0x80, 0x100
+BF_FLAG_KEY_BUFFER = 0x200
 
 
 class bf_options(ctypes.Structure):
@@ -73,6 +74,8 @@ _sig = {
     "bf_last_error": (ctypes.c_char_p, []),
 }
 for _name, (_res, _args) in _sig.items():
+    if os.environ.get("BF_LIB") and not hasattr(_lib, _name):
+        continue  # an older build under A/B comparison (tools/ab.sh) may lack newer entry points
     _f = getattr(_lib, _name)
     _f.restype, _f.argtypes = _res, _args
 

@@ -35,8 +35,22 @@ __device__ __forceinline__ void add_degree(uint32_t* deg, uint32_t z, bool valid
   if ((threadIdx.x & 31) == (uint32_t)(__ffs(peers) - 1)) atomicAdd(&deg[z], (uint32_t)__popc(peers));
 }
 
+// Degree counting privatises what it can: a side of at most HIST_MAX vertices
+// (c4: 30K items with Zipf popularity -- millions of increments on a few
+// addresses) is counted in a per-CTA shared-memory histogram and flushed once
+// per CTA; the other side's increments go to one of `stripes` copies of the
+// degree array (chosen by CTA; copy 0 is deg itself, summed by
+// k_degree_stripes), so a hub's increments spread over several addresses.
+constexpr uint32_t HIST_MAX = 40960;
+
 __global__ void k_validate_degree(const uint32_t* __restrict__ e, uint64_t m, uint32_t nU, uint32_t nV,
-                                  uint32_t* __restrict__ deg, uint32_t* __restrict__ flags) {
+                                  uint32_t* __restrict__ deg, uint32_t* __restrict__ flags, int hist_side,
+                                  uint32_t stripes, uint64_t n) {
+  extern __shared__ uint32_t hist[];
+  const uint32_t nh = hist_side == 0 ? nU : hist_side == 1 ? nV : 0u;
+  for (uint32_t i = threadIdx.x; i < nh; i += blockDim.x) hist[i] = 0;
+  __syncthreads();
+  uint32_t* dg = deg + (size_t)(blockIdx.x % stripes) * n;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   // warp-uniform trip count (the aggregation is a warp collective)
   for (uint64_t i0 = blockIdx.x * (uint64_t)blockDim.x + (threadIdx.x & ~31u); i0 < m; i0 += stride) {
@@ -48,8 +62,22 @@ __global__ void k_validate_degree(const uint32_t* __restrict__ e, uint64_t m, ui
       ok = uv.x < nU && uv.y < nV;
       if (!ok) atomicOr(flags, 1u);
     }
-    add_degree(deg, uv.x, ok);
-    add_degree(deg, nU + uv.y, ok);
+    if (hist_side == 0) { if (ok) atomicAdd(&hist[uv.x], 1u); }
+    else add_degree(dg, uv.x, ok);
+    if (hist_side == 1) { if (ok) atomicAdd(&hist[uv.y], 1u); }
+    else add_degree(dg, nU + uv.y, ok);
+  }
+  __syncthreads();
+  const uint32_t base = hist_side == 1 ? nU : 0u;
+  for (uint32_t i = threadIdx.x; i < nh; i += blockDim.x)
+    if (hist[i]) atomicAdd(&deg[base + i], hist[i]);
+}
+
+__global__ void k_degree_stripes(uint32_t* __restrict__ deg, uint64_t n, uint32_t stripes) {
+  for (uint64_t z = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; z < n; z += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t d = deg[z];
+    for (uint32_t s = 1; s < stripes; s++) d += deg[(size_t)s * n + z];
+    deg[z] = d;
   }
 }
 
@@ -226,30 +254,12 @@ __global__ void k_slot_keys(const uint32_t* __restrict__ e, uint64_t m, uint32_t
     uint2 uv = reinterpret_cast<const uint2*>(e)[i];
     uint64_t ru = rid_of_gid[uv.x], rv = rid_of_gid[(uint64_t)nU + uv.y];
     const uint64_t ku = (ru << Bv) | (n - 1 - rv);                    // nbr_last = n-1
-    const uint64_t kv = ((rv - nU) << Bu) | ((uint64_t)nU - 1 - ru);  // nbr_last = nU-1, src_base = nU
     if (Be) {
       keys[i] = (ku << Be) | i;
-      keys[m + i] = (kv << Be) | i;
     } else {
       keys[i] = ku;
-      keys[m + i] = kv;
-      vals[i] = (uint32_t)(2 * i);
-      vals[m + i] = (uint32_t)(2 * i + 1);
+      vals[i] = (uint32_t)i;
     }
-  }
-}
-
-// pos[x->y] = index of x in N(y) (the twin slot's offset in y's row); also
-// rejects repeated edges: after the slot sort a repeated (u,v) pair is two
-// adjacent equal slots of the same source (reading Z8)
-__global__ void k_pos(const uint32_t* __restrict__ vals, const uint32_t* __restrict__ where,
-                      const uint32_t* __restrict__ nbr, const uint32_t* __restrict__ src,
-                      const uint32_t* __restrict__ off, uint64_t S, uint32_t* __restrict__ pos,
-                      uint32_t* __restrict__ flags) {
-  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < S; j += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t y = nbr[j];
-    if (j + 1 < S && nbr[j + 1] == y && src[j + 1] == src[j]) atomicOr(flags, 2u);
-    pos[j] = where[vals[j] ^ 1u] - off[y];
   }
 }
 
@@ -273,12 +283,16 @@ __global__ void k_hi(const uint32_t* __restrict__ nbr, const uint32_t* __restric
 
 // per-slot wedge segment under the orientation (a4): the segment of N(y) that
 // slot (x -> y) retrieves, as (first index in nbr, length)
+// also rejects repeated edges (reading Z8): a repeated (u,v) pair is two
+// adjacent equal slots of the ranked U half
 __global__ void k_wslot(const uint32_t* __restrict__ nbr, const uint32_t* __restrict__ src,
                         const uint32_t* __restrict__ pos, const uint32_t* __restrict__ off,
                         const uint32_t* __restrict__ hi, uint64_t S, int orient, uint32_t* __restrict__ seglo,
-                        uint32_t* __restrict__ seglen) {
+                        uint32_t* __restrict__ seglen, uint32_t* __restrict__ flags) {
+  bool dup = false;
   for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < S; j += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t x = src[j], y = nbr[j];
+    if (j + 1 < S / 2 && nbr[j + 1] == y && src[j + 1] == x) dup = true;
     uint32_t lo, len;
     if (orient == BF_ORIENT_LOW) {
       // Alg. 2: slot i < deg_x(x) retrieves N(y)[0 : deg_x(y)), deg_x(y) = pos
@@ -295,6 +309,7 @@ __global__ void k_wslot(const uint32_t* __restrict__ nbr, const uint32_t* __rest
     seglo[j] = lo;
     seglen[j] = len;
   }
+  if (dup) atomicOr(flags, 2u);
 }
 
 __global__ void k_items(const uint32_t* __restrict__ order, uint32_t cnt, const uint32_t* __restrict__ off,
@@ -405,9 +420,14 @@ static bf_status plan_split(bf_graph* g);
 bf_status graph_ingest(bf_graph* g, const uint32_t* edges) {
   cudaStream_t s = g->stream;
   uint64_t m = g->m, n = g->n;
+  // degree stripes: as many copies as fit 64 MB (at most 8), none for a tiny graph
+  uint32_t stripes = 1;
+  while (stripes < 8 && n * 4 * (stripes * 2) <= ((size_t)64 << 20) && m >= ((uint64_t)1 << 20)) stripes *= 2;
+  const int hist_side = g->n_v <= HIST_MAX && g->n_v <= g->n_u ? 1 : (g->n_u <= HIST_MAX ? 0 : -1);
+  const uint32_t nh = hist_side == 0 ? g->n_u : hist_side == 1 ? g->n_v : 0u;
   g->edges.ensure(std::max<uint64_t>(m, 1) * 8);
-  g->deg.ensure(std::max<uint64_t>(n, 1) * 4);
-  CUDA_TRY(cudaMemsetAsync(g->deg.p, 0, std::max<uint64_t>(n, 1) * 4, s));
+  g->deg.ensure(std::max<uint64_t>(n, 1) * 4 * stripes);
+  CUDA_TRY(cudaMemsetAsync(g->deg.p, 0, std::max<uint64_t>(n, 1) * 4 * stripes, s));
   if (m) {
     CUDA_TRY(cudaMemcpyAsync(g->edges.p, edges, m * 8,
                              g->opt.edges_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
@@ -416,9 +436,20 @@ bf_status graph_ingest(bf_graph* g, const uint32_t* edges) {
   uint32_t* flags = g->tmp_a.as<uint32_t>();
   CUDA_TRY(cudaMemsetAsync(flags, 0, 4, s));
   if (m) {
-    k_validate_degree<<<grid_for(m, g->sms), TPB, 0, s>>>(g->edges.as<uint32_t>(), m, g->n_u, g->n_v,
-                                                          g->deg.as<uint32_t>(), flags);
+    const size_t smem = (size_t)nh * 4;
+    const int threads = 1024;
+    CUDA_TRY(cudaFuncSetAttribute(k_validate_degree, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_validate_degree, threads, smem));
+    const uint64_t want = (m + threads - 1) / threads;
+    const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)g->sms * std::max(per_sm, 1)));
+    k_validate_degree<<<grid, threads, smem, s>>>(g->edges.as<uint32_t>(), m, g->n_u, g->n_v, g->deg.as<uint32_t>(),
+                                                  flags, hist_side, stripes, n);
     KERNEL_CHECK(g);
+    if (stripes > 1) {
+      k_degree_stripes<<<grid_for(n, g->sms), TPB, 0, s>>>(g->deg.as<uint32_t>(), n, stripes);
+      KERNEL_CHECK(g);
+    }
   }
   uint32_t hflags = 0;
   CUDA_TRY(cudaMemcpyAsync(&hflags, flags, 4, cudaMemcpyDeviceToHost, s));
@@ -518,7 +549,7 @@ bf_status graph_rank(bf_graph* g, int kind) {
   g->wstart.ensure(n1 * 8);
   g->nbr.ensure(S1 * 4);
   g->pos.ensure(S1 * 4);
-  g->where.ensure(S1 * 4);
+  g->eid.ensure(std::max<uint64_t>(m, 1) * 4);
   // scratch
   size_t big = std::max<size_t>(S1, n1);
   g->tmp_a.ensure(big * 8 + 64);            // keys0 (u64)
@@ -583,17 +614,17 @@ bf_status graph_rank(bf_graph* g, int kind) {
                                                      g->rid_of_gid.as<uint32_t>(), k0, v0);
     KERNEL_CHECK(g);
     uint32_t* src = g->tmp_f.as<uint32_t>();
-    uint32_t* where = g->where.as<uint32_t>();
     uint32_t* nbr = g->nbr.as<uint32_t>();
-    // U half: nbr = (n-1) - low, src = high; V half: nbr = (nU-1) - low, src = nU + high
-    const int wu = radix_sort_slots(k0, v0, k1, v1, m, Bu + Bv, Bv, Be, 0, n - 1, 0, 0, nbr, src, where, tmp, s, L);
-    const int wv = radix_sort_slots(k0 + m, v0 + m, k1 + m, v1 + m, m, Bu + Bv, Bu, Be, 1, (uint64_t)g->n_u - 1,
-                                    g->n_u, m, nbr + m, src + m, where, tmp, s, L);
-    if (wu != wv) CUDA_TRY(cudaMemcpyAsync(wu ? v0 : v1, wu ? v1 : v0, m * 4, cudaMemcpyDeviceToDevice, s));
-    uint32_t* vs = wv ? v1 : v0;  // slot ids in CSR order
-    k_pos<<<grid_for(S, g->sms), TPB, 0, s>>>(vs, where, nbr, src, g->off.as<uint32_t>(), S, g->pos.as<uint32_t>(),
-                                               g->dflag.as<uint32_t>());
-    KERNEL_CHECK(g);
+    // U half: nbr = (n-1) - low, src = high, sorted over all its bits; its last
+    // pass also lays out the V half's records transposed and reversed, already
+    // in descending-u order, so the V half sorts over its v field only (Bv bits
+    // instead of Bu + Bv) and its last pass writes both twins' pos (Alg. 1
+    // l.5-6).  V half: nbr = (nU-1) - low, src = nU + high.
+    const SlotTranspose tr = {k0 + m, v0 + m, g->n_u, Bu};
+    radix_sort_slots(k0, v0, k1, v1, m, Bu + Bv, 0, Bv, Be, n - 1, 0, 0, nbr, src, g->eid.as<uint32_t>(), nullptr,
+                     nullptr, &tr, tmp, s, L);
+    radix_sort_slots(k0 + m, v0 + m, k1 + m, v1 + m, m, Bu + Bv, Bu, Bu, Be, (uint64_t)g->n_u - 1, g->n_u, m,
+                     nbr + m, src + m, nullptr, g->pos.as<uint32_t>(), g->off.as<uint32_t>(), nullptr, tmp, s, L);
   }
   if (n) {
     k_hi<<<grid_for(n, g->sms), TPB, 0, s>>>(g->nbr.as<uint32_t>(), g->off.as<uint32_t>(), g->rkey.as<uint64_t>(), n,
@@ -621,7 +652,7 @@ bf_status graph_plan(bf_graph* g) {
   if (m) {
     k_wslot<<<grid_for(S, g->sms), TPB, 0, s>>>(g->nbr.as<uint32_t>(), src, g->pos.as<uint32_t>(),
                                                  g->off.as<uint32_t>(), g->hi.as<uint32_t>(), S, g->orient,
-                                                 g->seglo.as<uint32_t>(), wslot);
+                                                 g->seglo.as<uint32_t>(), wslot, g->dflag.as<uint32_t>());
     KERNEL_CHECK(g);
   }
   scan_exclusive_u32_u64(wslot, wpre, S, wpre + S, tmp, s, L);

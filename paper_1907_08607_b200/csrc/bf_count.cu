@@ -77,6 +77,9 @@ struct CountArgs {
   uint32_t exp;           // libbf_prof.so only: timing experiments (env BF_EXPERIMENT; results are wrong when set):
                           // 1 = skip endpoint REDs, 2 = skip centre REDs
   uint32_t win;           // dense window keys in use (<= compile-time size)
+  uint32_t dwin;          // dense variant (WIN == 0): window keys (>= every heavy start's key range)
+  uint32_t* kbuf;         // slot-mode key buffer [W] (vertex mode, mostly-short-segment graphs) or null
+  uint32_t short_segs;    // the graph's segments are short on average: slot mode keeps SB slots in flight
   uint32_t cap;           // heavy chunk capacity in wedges (<= HV_CAP)
   int rank, world;
 };
@@ -260,11 +263,11 @@ struct HeavyStore {
 // d-1 stay in registers until one shared atomic per unit.
 template <int NT, uint32_t UCAP>
 struct Units {
-  static_assert(NT <= 256, "unit meta packs the slot in 8 bits");
+  static_assert(NT <= 2048, "unit meta packs the slot in 11 bits");
   using SlotT = typename std::conditional<(NT <= 256), uint8_t, uint16_t>::type;
   uint32_t lo[UCAP];           // first nbr index of the unit
   uint32_t meta[UCAP];         // chunk position of the first wedge (key cache index, bits 0-15)
-                               // | length 1..P (bits 16-23) | chunk-local slot (bits 24-31)
+                               // | length - 1 in 0..P-1 (bits 16-20) | chunk-local slot (bits 21-31)
   uint32_t slo[NT], shi[NT];   // pass-2 per-slot sums (u64 as two u32)
   uint32_t wt[32];             // scan scratch
   uint32_t jn[2];              // continuation slot of chunk i in jn[i & 1] (FULL = none)
@@ -294,6 +297,7 @@ __device__ __forceinline__ void cta_sync() {
 // write the units of one slot segment [lo, lo+L) (thread t), then barrier
 template <int NT, int P, uint32_t UCAP>
 __device__ __forceinline__ void units_write(Units<NT, UCAP>& u, uint32_t lo, uint32_t L) {
+  static_assert(P <= 32 && (P & (P - 1)) == 0, "unit length is packed in 5 bits");
   constexpr uint32_t LP = 31 - __builtin_clz(P);
   const uint32_t nu = (L + P - 1) >> LP;
   uint32_t total;
@@ -303,7 +307,7 @@ __device__ __forceinline__ void units_write(Units<NT, UCAP>& u, uint32_t lo, uin
   BF_CHECK(ex + nu <= UCAP && L < 65536);
   for (uint32_t f = 0, o = 0; f < nu; f++, o += P) {
     u.lo[ex + f] = lo + o;
-    u.meta[ex + f] = ((wp + o) & 0xffffu) | ((f + 1 < nu ? (uint32_t)P : L - o) << 16) | (threadIdx.x << 24);
+    u.meta[ex + f] = ((wp + o) & 0xffffu) | ((f + 1 < nu ? (uint32_t)P - 1 : L - o - 1) << 16) | (threadIdx.x << 21);
   }
   if (threadIdx.x == 0) u.nunits = total & 0xffffu;
   u.slo[threadIdx.x] = 0;
@@ -349,10 +353,22 @@ __device__ __forceinline__ uint64_t units_build(const CountArgs& a, Units<NT, UC
 // (shared memory up to lcap entries, then the CTA's global list)
 // SPILL: the list can outgrow shared memory (heavy tier); otherwise lcap is
 // an exact bound (small tiers: distinct keys <= w <= lcap)
+// BF_LIST_AGG: warp-aggregated push (the lanes pushing together take one
+// atomicAdd on the list counter) -- a tuning experiment, off by default
+#ifndef BF_LIST_AGG
+#define BF_LIST_AGG 0
+#endif
 template <bool SPILL>
 __device__ __forceinline__ void list_push(uint32_t* lcnt, uint32_t* list, uint32_t lcap, uint32_t* olist,
                                           uint64_t ocap, uint32_t key) {
+#if BF_LIST_AGG
+  const uint32_t am = __activemask(), lane = threadIdx.x & 31u, leader = __ffs(am) - 1u;
+  uint32_t base = 0;
+  if (lane == leader) base = atomicAdd(lcnt, (uint32_t)__popc(am));
+  const uint32_t i = __shfl_sync(am, base, leader) + (uint32_t)__popc(am & ((1u << lane) - 1u));
+#else
   const uint32_t i = atomicAdd(lcnt, 1u);
+#endif
   if (!SPILL || i < lcap) list[i] = key;
   else {
     BF_CHECK(olist != nullptr && i - lcap < ocap);
@@ -379,7 +395,7 @@ __device__ __forceinline__ void units_pass1(const CountArgs& a, Units<NT, UCAP>&
     for (int r = 0; r < UR; r++) {
       const uint32_t x = x0 + r * NG;
       const uint32_t lo = x < nunits ? u.lo[x] : 0u, me = x < nunits ? u.meta[x] : 0u;
-      const uint32_t len = (me >> 16) & 0xffu;
+      const uint32_t len = x < nunits ? ((me >> 16) & 31u) + 1 : 0u;
       ps[r] = me & 0xffffu;
 #pragma unroll
       for (int it = 0; it < IT; it++) {
@@ -422,9 +438,9 @@ __device__ __forceinline__ void units_pass2(const CountArgs& a, Units<NT, UCAP>&
       const uint32_t x = xb + r * NG + (tid & 31) / G;
       const bool act = x < nunits;
       lo[r] = act ? u.lo[x] : 0u;
-      const uint32_t me = act ? u.meta[x] : 0u, len = (me >> 16) & 0xffu;
+      const uint32_t me = act ? u.meta[x] : 0u, len = act ? ((me >> 16) & 31u) + 1 : 0u;
       ps[r] = me & 0xffffu;
-      sl[r] = me >> 24;
+      sl[r] = me >> 21;
 #pragma unroll
       for (int it = 0; it < IT; it++) {
         const uint32_t i = gl + it * G;
@@ -584,46 +600,120 @@ __device__ __forceinline__ void start_passes(const CountArgs& a, Units<NT, UCAP>
 #ifndef BF_SLOT_MODE_AVG
 #define BF_SLOT_MODE_AVG 16
 #endif
-constexpr uint32_t SLOT_MODE_AVG = BF_SLOT_MODE_AVG;  // slot mode when w < SLOT_MODE_AVG * #slots (measured: 6 -> 16 takes c4 50.6 -> 38.5 ms)
+constexpr uint32_t SLOT_MODE_AVG = BF_SLOT_MODE_AVG;
+constexpr uint64_t kKeyBufMax = (uint64_t)2 << 30;  // keys (8 GB)  // slot mode when w < SLOT_MODE_AVG * #slots (measured: 6 -> 16 takes c4 50.6 -> 38.5 ms)
 
-template <bool SPILL, int NT, class Store>
+// Each thread keeps SB slots in flight (strided by NT): their (lo, len) pairs,
+// then up to four keys of each -- SB independent random N(y) reads per thread,
+// the memory-level parallelism that short random segments need.  With a key
+// buffer (a.kbuf, vertex mode, graphs of mostly short segments) pass 1 also
+// stores each segment's keys at kbuf[wpre[j] + i] -- the wedge's global index --
+// so pass 2 reads them back sequentially instead of gathering N(y) again.
+// (SB = 4 only on graphs of short segments, a separate kernel instance: the
+// four-slot code in the same kernel cost c2 0.35 ms through register pressure.)
+template <bool SPILL, int NT, int SB, class Store>
 __device__ __forceinline__ void slots_pass1(const CountArgs& a, const Store& cs, uint32_t j0, uint32_t j1,
                                             uint32_t kbase, uint32_t* lcnt, uint32_t* list, uint32_t lcap,
                                             uint32_t* olist, bool& hashed) {
-  for (uint32_t j = j0 + threadIdx.x; j < j1; j += NT) {
-    const uint32_t len = __ldg(a.seglen + j), lo = __ldg(a.seglo + j);
-    for (uint32_t i0 = 0; i0 < len; i0 += 4) {
-      uint32_t k[4];
+  for (uint32_t jb = j0 + threadIdx.x; jb < j1; jb += NT * SB) {
+    uint32_t lo[SB], len[SB], k[SB][4];
 #pragma unroll
-      for (int t = 0; t < 4; t++) k[t] = i0 + t < len ? __ldg(a.nbr + (lo + i0 + t)) : EMPTY;
+    for (int b = 0; b < SB; b++) {
+      const uint32_t j = jb + b * NT;
+      len[b] = j < j1 ? __ldg(a.seglen + j) : 0u;
+      lo[b] = j < j1 ? __ldg(a.seglo + j) : 0u;
+    }
+#pragma unroll
+    for (int b = 0; b < SB; b++)
+#pragma unroll
+      for (int t = 0; t < 4; t++) k[b][t] = t < (int)len[b] ? __ldg(a.nbr + (lo[b] + t)) : EMPTY;
+    if (a.kbuf) {
+#pragma unroll
+      for (int b = 0; b < SB; b++)
+        if (len[b]) {
+          uint32_t* kb = a.kbuf + __ldg(a.wpre + jb + b * NT);
+#pragma unroll
+          for (int t = 0; t < 4; t++)
+            if (t < (int)len[b]) kb[t] = k[b][t];
+        }
+    }
+#pragma unroll
+    for (int b = 0; b < SB; b++)
 #pragma unroll
       for (int t = 0; t < 4; t++)
-        if (k[t] != EMPTY && cs.add(k[t], k[t] - kbase, hashed)) list_push<SPILL>(lcnt, list, lcap, olist, a.olist_len, k[t]);
+        if (k[b][t] != EMPTY && cs.add(k[b][t], k[b][t] - kbase, hashed))
+          list_push<SPILL>(lcnt, list, lcap, olist, a.olist_len, k[b][t]);
+    // the rest of segments longer than four
+#pragma unroll 1
+    for (int b = 0; b < SB; b++) {
+      if (len[b] <= 4) continue;
+      uint32_t* kb = a.kbuf ? a.kbuf + __ldg(a.wpre + jb + b * NT) : nullptr;
+      for (uint32_t i0 = 4; i0 < len[b]; i0 += 4) {
+        uint32_t kk[4];
+#pragma unroll
+        for (int t = 0; t < 4; t++) kk[t] = i0 + t < len[b] ? __ldg(a.nbr + (lo[b] + i0 + t)) : EMPTY;
+#pragma unroll
+        for (int t = 0; t < 4; t++)
+          if (kk[t] != EMPTY) {
+            if (kb) kb[i0 + t] = kk[t];
+            if (cs.add(kk[t], kk[t] - kbase, hashed)) list_push<SPILL>(lcnt, list, lcap, olist, a.olist_len, kk[t]);
+          }
+      }
     }
   }
 }
 
-template <int MODE, int NT, class Store>
+template <int MODE, int NT, int SB, class Store>
 __device__ __forceinline__ void slots_pass2(const CountArgs& a, const Store& cs, uint32_t j0, uint32_t j1,
-                                            uint32_t kbase) {
-  for (uint32_t j = j0 + threadIdx.x; j < j1; j += NT) {
-    const uint32_t len = __ldg(a.seglen + j), lo = __ldg(a.seglo + j);
-    uint64_t s = 0;
-    for (uint32_t i0 = 0; i0 < len; i0 += 4) {
-      uint32_t k[4];
+                                               uint32_t kbase) {
+  const bool kb = MODE == MODE_VERTEX && a.kbuf != nullptr;  // keys from the key buffer
+  for (uint32_t jb = j0 + threadIdx.x; jb < j1; jb += NT * SB) {
+    uint32_t lo[SB], len[SB], k[SB][4];
+    uint64_t s[SB];
 #pragma unroll
-      for (int t = 0; t < 4; t++) k[t] = i0 + t < len ? __ldg(a.nbr + (lo + i0 + t)) : EMPTY;
+    for (int b = 0; b < SB; b++) {
+      const uint32_t j = jb + b * NT;
+      len[b] = j < j1 ? __ldg(a.seglen + j) : 0u;
+      lo[b] = 0u;
+      if (j < j1) lo[b] = kb ? 0u : __ldg(a.seglo + j);
+      s[b] = 0;
+    }
+    const uint32_t* src[SB];
+#pragma unroll
+    for (int b = 0; b < SB; b++) src[b] = kb ? (len[b] ? a.kbuf + __ldg(a.wpre + jb + b * NT) : a.kbuf) : a.nbr + lo[b];
+#pragma unroll
+    for (int b = 0; b < SB; b++)
+#pragma unroll
+      for (int t = 0; t < 4; t++) k[b][t] = t < (int)len[b] ? (kb ? __ldcs(src[b] + t) : __ldg(src[b] + t)) : EMPTY;
+#pragma unroll
+    for (int b = 0; b < SB; b++)
 #pragma unroll
       for (int t = 0; t < 4; t++)
-        if (k[t] != EMPTY) {
-          const uint32_t c = cs.get(k[t], k[t] - kbase) - 1u;
-          s += c;
-          if (MODE == MODE_EDGE && c) red_add_u64(a.acc + (lo + i0 + t), c);  // edge (y, key)
+        if (k[b][t] != EMPTY) {
+          const uint32_t c = cs.get(k[b][t], k[b][t] - kbase) - 1u;
+          s[b] += c;
+          if (MODE == MODE_EDGE && c) red_add_u64(a.acc + (lo[b] + t), c);  // edge (y, key)
         }
-    }
-    if (s) {
-      if (MODE == MODE_VERTEX) { if (!(a.exp & 2)) red_add_u64(a.bv + __ldg(a.nbr + j), s); }  // centre y
-      else red_add_u64(a.acc + j, s);                                                        // edge (s, y)
+#pragma unroll 1
+    for (int b = 0; b < SB; b++) {
+      for (uint32_t i0 = 4; i0 < len[b]; i0 += 4) {
+        uint32_t kk[4];
+#pragma unroll
+        for (int t = 0; t < 4; t++)
+          kk[t] = i0 + t < len[b] ? (kb ? __ldcs(src[b] + i0 + t) : __ldg(src[b] + i0 + t)) : EMPTY;
+#pragma unroll
+        for (int t = 0; t < 4; t++)
+          if (kk[t] != EMPTY) {
+            const uint32_t c = cs.get(kk[t], kk[t] - kbase) - 1u;
+            s[b] += c;
+            if (MODE == MODE_EDGE && c) red_add_u64(a.acc + (lo[b] + i0 + t), c);  // edge (y, key)
+          }
+      }
+      const uint32_t j = jb + b * NT;
+      if (s[b]) {
+        if (MODE == MODE_VERTEX) { if (!(a.exp & 2)) red_add_u64(a.bv + __ldg(a.nbr + j), s[b]); }  // centre y
+        else red_add_u64(a.acc + j, s[b]);                                                         // edge (s, y)
+      }
     }
   }
 }
@@ -747,11 +837,18 @@ struct HeavySmemT {
   uint32_t win[WIN];
   uint32_t list[LCAP];
 };
+// split starts whose key ranges all fit DENSE_MAX_KEYS (c4: 30K items) are
+// counted in a shared window over the whole key range -- the paper's
+// simple-batching array of every possible second endpoint held on
+// chip -- so no key of a piece takes the global row in pass 1.  (The same
+// window for the heavy tier, one 1024-thread CTA per SM, measured slower on c4
+// than four 256-thread CTAs with a 4096-key window: 7.3 against 5.5 ms.)
+constexpr uint32_t DENSE_MAX_KEYS = 40960;
 
 #ifndef BF_BIG_MINB
-#define BF_BIG_MINB 1
+#define BF_BIG_MINB 4  // <= 64 registers: four 256-thread CTAs per SM (the shared-memory limit too)
 #endif
-template <int ORIENT, int MODE, int NT, uint32_t WIN, uint32_t CAP, uint32_t LCAP, int P, int G, int UR>
+template <int ORIENT, int MODE, int SB, int NT, uint32_t WIN, uint32_t CAP, uint32_t LCAP, int P, int G, int UR>
 __global__ void __launch_bounds__(NT, BF_BIG_MINB) k_big(CountArgs a) {
   using SM = HeavySmemT<NT, WIN, CAP, LCAP, P, G, UR>;
   extern __shared__ __align__(16) char sm[];
@@ -782,14 +879,14 @@ __global__ void __launch_bounds__(NT, BF_BIG_MINB) k_big(CountArgs a) {
     bool hashed = false;
     pf.mark(0);
     if (w < (uint64_t)SLOT_MODE_AVG * (st.j1 - st.j0)) {  // short segments: slot mode
-      slots_pass1<true, NT>(a, cs, st.j0, st.j1, st.kbase, &hs.u.lcnt, hs.list, LCAP, olist, hashed);
+      slots_pass1<true, NT, SB>(a, cs, st.j0, st.j1, st.kbase, &hs.u.lcnt, hs.list, LCAP, olist, hashed);
       __syncthreads();
       const uint32_t cnt = hs.u.lcnt;
       list_finalize<MODE, true, NT>(a, cs, st.kbase, cnt, hs.list, LCAP, olist, lsum);
       if (tid == 0) pair_acc += cnt;
       __syncthreads();
       if (MODE != MODE_TOTAL) {
-        slots_pass2<MODE, NT>(a, cs, st.j0, st.j1, st.kbase);
+        slots_pass2<MODE, NT, SB>(a, cs, st.j0, st.j1, st.kbase);
         __syncthreads();
       }
       for (uint32_t i = tid; i < cnt; i += NT) {
@@ -857,30 +954,50 @@ struct SplitStore1 {
     return false;
   }
 };
+// dense variant: every key is in the shared window; owners are not tracked
+// (the flush scans the window)
+struct SplitStore1Dense {
+  uint32_t* win;
+  __device__ __forceinline__ bool add(uint32_t, uint32_t kk, bool&) const {
+    atomicAdd(win + kk, 1u);
+    return false;
+  }
+};
 struct SplitStore2 {
   const uint32_t* row;
   __device__ __forceinline__ uint32_t get(uint32_t, uint32_t kk) const { return __ldcg(row + kk); }
 };
 
-constexpr int SP_NT = 256;
+constexpr int SP_NT = 256;    // pass 1 with the 8192-key window + owner list
+constexpr int SP_NT_WIDE = 1024;  // dense pass 1 (one CTA per SM around the whole-key window) and pass 2
 constexpr uint32_t SP_WIN = 8192, SP_CAP = 8192;
 constexpr int SP_P = 32, SP_G = 4;
-struct SplitSmem {
-  static constexpr uint32_t UCAP = SP_CAP / SP_P + SP_NT;
-  Units<SP_NT, UCAP> u;
+template <int NT>
+struct SplitSmemT {
+  static constexpr uint32_t UCAP = SP_CAP / SP_P + NT;
+  using U = Units<NT, UCAP>;
+  U u;
   uint32_t win[SP_WIN];
   uint32_t list[SP_WIN];  // window owners of the piece (distinct window keys <= SP_WIN)
 };
 
-template <int ORIENT, int MODE, bool PASS2>
-__global__ void __launch_bounds__(SP_NT, 1) k_split_walk(CountArgs a, SplitArgs sa) {
+// DENSE: the window covers every key of every split start (a.dwin keys of
+// dynamic shared memory after the unit table; no owner list)
+// NT == SP_NT_WIDE runs with only the unit table in shared memory (pass 2) or
+// the unit table plus the dense window (pass 1, DENSE): win / list of the
+// struct are never touched then.
+template <int ORIENT, int MODE, bool PASS2, bool DENSE, int NT>
+__global__ void __launch_bounds__(NT, NT == SP_NT ? 3 : 1) k_split_walk(CountArgs a, SplitArgs sa) {
   extern __shared__ __align__(16) char sm[];
+  using SplitSmem = SplitSmemT<NT>;
   SplitSmem& ss = *(SplitSmem*)sm;
-  using U = Units<SP_NT, SplitSmem::UCAP>;
+  using U = typename SplitSmem::U;
   const uint32_t tid = threadIdx.x;
   const uint32_t cap = min(a.cap, SP_CAP);
+  uint32_t* win = DENSE ? (uint32_t*)(sm + sizeof(U)) : ss.win;
+  const uint32_t wl = DENSE ? a.dwin : min(a.win, SP_WIN);
   if (!PASS2)
-    for (uint32_t i = tid; i < SP_WIN; i += SP_NT) ss.win[i] = 0;
+    for (uint32_t i = tid; i < wl; i += NT) win[i] = 0;
   if (tid == 0) { ss.u.jn[0] = ss.u.jn[1] = FULL; ss.u.lcnt = 0; }
   for (;;) {
     if (tid == 0) ss.u.item = sa.p0 + atomicAdd(a.queue, 1u);
@@ -894,46 +1011,59 @@ __global__ void __launch_bounds__(SP_NT, 1) k_split_walk(CountArgs a, SplitArgs 
     const uint32_t kbase = split_kbase<ORIENT>(a, sp.x);
     uint32_t* row = sa.rows + __ldg(sa.off + pc.x);
     uint32_t* glist = sa.lists + __ldg(sa.off + pc.x);
-    SplitStore1 s1{ss.win, min(a.win, SP_WIN), row, glist, sa.cnt + pc.x};
+    SplitStore1 s1{win, wl, row, glist, sa.cnt + pc.x};
+    SplitStore1Dense s1d{win};
     SplitStore2 s2{row};
     const uint64_t base = __ldg(a.wpre + pc.y), w = __ldg(a.wpre + pc.z) - base;
     uint32_t jc = pc.y, par = 0;
     uint64_t K0 = 0;
     bool hashed = false;
     if (w < (uint64_t)SLOT_MODE_AVG * (pc.z - pc.y)) {  // short segments: slot mode
-      if (PASS2) slots_pass2<MODE, SP_NT>(a, s2, pc.y, pc.z, kbase);
-      else slots_pass1<false, SP_NT>(a, s1, pc.y, pc.z, kbase, &ss.u.lcnt, ss.list, SP_WIN, nullptr, hashed);
+      if (PASS2) slots_pass2<MODE, NT, 4>(a, s2, pc.y, pc.z, kbase);
+      else if (DENSE) slots_pass1<false, NT, 4>(a, s1d, pc.y, pc.z, kbase, &ss.u.lcnt, ss.list, SP_WIN, nullptr, hashed);
+      else slots_pass1<false, NT, 4>(a, s1, pc.y, pc.z, kbase, &ss.u.lcnt, ss.list, SP_WIN, nullptr, hashed);
       __syncthreads();
       K0 = w;  // skip the unit walk
     }
     while (K0 < w) {
       bool mine;
       uint32_t myj, myy;
-      const uint64_t K1 = units_build<PASS2 ? MODE : MODE_TOTAL, SP_NT, SP_P, SplitSmem::UCAP>(
+      const uint64_t K1 = units_build<PASS2 ? MODE : MODE_TOTAL, NT, SP_P, SplitSmem::UCAP>(
           a, ss.u, jc, pc.z, base, K0, cap, par, mine, myj, myy);
       const uint32_t jn = ss.u.jn[par];
       if (PASS2) {
         if (sp.z - sp.y < (1u << 26))
-          units_pass2<MODE, false, SP_NT, SP_P, SP_G, 1, SplitSmem::UCAP>(a, ss.u, s2, kbase, nullptr);
+          units_pass2<MODE, false, NT, SP_P, SP_G, 1, SplitSmem::UCAP>(a, ss.u, s2, kbase, nullptr);
         else
-          units_pass2<MODE, false, SP_NT, SP_P, SP_G, 1, SplitSmem::UCAP, SplitStore2, false>(a, ss.u, s2, kbase,
+          units_pass2<MODE, false, NT, SP_P, SP_G, 1, SplitSmem::UCAP, SplitStore2, false>(a, ss.u, s2, kbase,
                                                                                              nullptr);
       }
-      else units_pass1<false, false, SP_NT, SP_P, SP_G, 1, SplitSmem::UCAP>(a, ss.u, s1, kbase, ss.list, SP_WIN, nullptr, hashed,
+      else if (DENSE)
+        units_pass1<false, false, NT, SP_P, SP_G, 1, SplitSmem::UCAP>(a, ss.u, s1d, kbase, ss.list, SP_WIN, nullptr,
+                                                                         hashed, nullptr);
+      else units_pass1<false, false, NT, SP_P, SP_G, 1, SplitSmem::UCAP>(a, ss.u, s1, kbase, ss.list, SP_WIN, nullptr, hashed,
                                                               nullptr);
       __syncthreads();
       if (tid == 0) ss.u.jn[par] = FULL;
       if (PASS2) slot_flush<MODE>(a, ss.u.slo, ss.u.shi, mine, myj, myy);
-      jc = jn != FULL ? jn : ((pc.z - jc > (uint32_t)SP_NT) ? jc + SP_NT : pc.z);
+      jc = jn != FULL ? jn : ((pc.z - jc > (uint32_t)NT) ? jc + NT : pc.z);
       K0 = K1;
       par ^= 1u;
     }
-    if (!PASS2) {  // flush the piece's window counts into the start's row
+    if (!PASS2 && DENSE) {  // flush the piece's window into the start's row (scan: no owner list)
+      for (uint32_t kk = tid; kk < wl; kk += NT) {
+        const uint32_t c = win[kk];
+        if (!c) continue;
+        win[kk] = 0;
+        if (atomicAdd(row + kk, c) == 0u) glist[atomicAdd(sa.cnt + pc.x, 1u)] = kk + kbase;
+      }
+      __syncthreads();
+    } else if (!PASS2) {  // flush the piece's window counts into the start's row
       const uint32_t cnt = ss.u.lcnt;
-      for (uint32_t i = tid; i < cnt; i += SP_NT) {
+      for (uint32_t i = tid; i < cnt; i += NT) {
         const uint32_t key = ss.list[i], kk = key - kbase;
-        const uint32_t c = ss.win[kk];
-        ss.win[kk] = 0;
+        const uint32_t c = win[kk];
+        win[kk] = 0;
         if (atomicAdd(row + kk, c) == 0u) glist[atomicAdd(sa.cnt + pc.x, 1u)] = key;
       }
       __syncthreads();
@@ -1099,12 +1229,13 @@ __global__ void k_unrename(const uint64_t* __restrict__ bv, const uint32_t* __re
   }
 }
 
-__global__ void k_edge_gather(const uint64_t* __restrict__ acc, const uint2* __restrict__ where, uint64_t m,
-                              uint64_t* __restrict__ be) {
-  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m; e += (uint64_t)gridDim.x * blockDim.x) {
-    const uint2 w = where[e];  // the edge's two slots
-    be[e] = acc[w.x] + acc[w.y];
-  }
+// be[e] = the sums of the edge's two slots: U-half position p and its twin
+// off[v] + pos[p] in v's row
+__global__ void k_edge_gather(const uint64_t* __restrict__ acc, const uint32_t* __restrict__ eid,
+                              const uint32_t* __restrict__ nbr, const uint32_t* __restrict__ pos,
+                              const uint32_t* __restrict__ off, uint64_t m, uint64_t* __restrict__ be) {
+  for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < m; p += (uint64_t)gridDim.x * blockDim.x)
+    be[eid[p]] = acc[p] + acc[(size_t)off[nbr[p]] + pos[p]];
 }
 
 inline unsigned grid_for(size_t n, int sms) {
@@ -1170,19 +1301,23 @@ void launch_tiers(bf_graph* g, CountArgs a, const uint32_t tier[4], uint32_t* qu
       sa.rows = g->srow.as<uint32_t>();
       sa.lists = g->slist.as<uint32_t>();
       sa.s0 = b.s0; sa.s1 = b.s1; sa.p0 = b.p0; sa.p1 = b.p1;
-      auto k1 = k_split_walk<ORIENT, MODE, false>;
-      const int grid = sms * occupancy(k1, SP_NT, sizeof(SplitSmem));
+      const bool dense = a.dwin != 0;
+      auto k1 = dense ? k_split_walk<ORIENT, MODE, false, true, SP_NT_WIDE> : k_split_walk<ORIENT, MODE, false, false, SP_NT>;
+      const int nt1 = dense ? SP_NT_WIDE : SP_NT;
+      const size_t smem = dense ? sizeof(SplitSmemT<SP_NT_WIDE>::U) + (size_t)a.dwin * 4 : sizeof(SplitSmemT<SP_NT>);
+      const int grid = sms * occupancy(k1, nt1, smem);
       const int fgrid = (int)std::min<uint32_t>(b.s1 - b.s0, (uint32_t)sms * 8);
       CUDA_TRY(cudaMemsetAsync(queues + 4, 0, 8, s));
       a.queue = queues + 4;
-      k1<<<grid, SP_NT, sizeof(SplitSmem), s>>>(a, sa);
+      k1<<<grid, nt1, smem, s>>>(a, sa);
       KERNEL_CHECK(g);
       k_split_finalize<ORIENT, MODE><<<fgrid, 256, 0, s>>>(a, sa);
       KERNEL_CHECK(g);
       if (MODE != MODE_TOTAL) {
-        auto k2 = k_split_walk<ORIENT, MODE, true>;
+        auto k2 = k_split_walk<ORIENT, MODE, true, false, SP_NT_WIDE>;  // pass 2 reads the global rows only
+        const size_t smem2 = sizeof(SplitSmemT<SP_NT_WIDE>::U);
         a.queue = queues + 5;
-        k2<<<sms * occupancy(k2, SP_NT, sizeof(SplitSmem)), SP_NT, sizeof(SplitSmem), s>>>(a, sa);
+        k2<<<sms * occupancy(k2, SP_NT_WIDE, smem2), SP_NT_WIDE, smem2, s>>>(a, sa);
         KERNEL_CHECK(g);
         k_split_clear<ORIENT><<<fgrid, 256, 0, s>>>(a, sa);
         KERNEL_CHECK(g);
@@ -1190,8 +1325,10 @@ void launch_tiers(bf_graph* g, CountArgs a, const uint32_t tier[4], uint32_t* qu
     }
   }
   if (tier[1] > tier[0] + g->n_split) {  // heavy
-    auto k = k_big<ORIENT, MODE, BIG_CFG>;
-    int grid = sms * occupancy(k, BF_BIG_NT, sizeof(BigSM));
+    auto k = a.short_segs ? k_big<ORIENT, MODE, 4, BIG_CFG> : k_big<ORIENT, MODE, 1, BIG_CFG>;
+    const int nt = BF_BIG_NT;
+    const size_t smem = sizeof(BigSM);
+    int grid = sms * occupancy(k, nt, smem);
     // one overflow row + touched list per CTA, from the device's row pool
     // (rows are kept zero by the owners' resets, so a clean pool is reused
     // across graphs without clearing); the grid shrinks if the rows of every
@@ -1221,7 +1358,7 @@ void launch_tiers(bf_graph* g, CountArgs a, const uint32_t tier[4], uint32_t* qu
     a.orow = (uint32_t*)pool.p;   // [grid][orow_len]
     a.olist = (uint32_t*)pool.l;  // [grid][olist_len]
     a.t0 = tier[0] + g->n_split; a.t1 = tier[1]; a.queue = queues + 0;
-    k<<<grid, BF_BIG_NT, sizeof(BigSM), s>>>(a);
+    k<<<grid, nt, smem, s>>>(a);
     KERNEL_CHECK(g);
   }
   if (tier[2] > tier[1]) {  // medium
@@ -1290,6 +1427,17 @@ bf_status graph_count(bf_graph* g, int mode, uint64_t* out_a, uint64_t* out_b, u
   a.total = dtot;
   a.orow = nullptr;
   a.olist = nullptr;
+  // split pieces count in a whole-key-range window when every heavy start's key range fits
+  const bool dense = olen <= DENSE_MAX_KEYS && win == 0xFFFFFFFFu && !(g->opt.test_flags & BF_FLAG_NO_DENSE_ROW);
+  a.dwin = dense ? (uint32_t)((olen + 3) & ~3ull) : 0u;
+  // slot-mode key buffer: vertex mode, graphs of mostly short segments (average
+  // wedges per slot below the slot-mode threshold), W keys within budget
+  a.kbuf = nullptr;
+  a.short_segs = g->W < (uint64_t)SLOT_MODE_AVG * S || (g->opt.test_flags & BF_FLAG_KEY_BUFFER);
+  if (mode == MODE_VERTEX && g->W && g->W <= kKeyBufMax && a.short_segs) {
+    g->kbuf.ensure(g->W * 4);
+    a.kbuf = g->kbuf.as<uint32_t>();
+  }
   const uint64_t hwl = std::min<uint64_t>(win, HV_WIN_KEYS);  // the heavy kernel's window in keys
   a.orow_len = olen > hwl ? olen - hwl : 1;
   a.olist_len = olen;
@@ -1369,8 +1517,9 @@ bf_status graph_count(bf_graph* g, int mode, uint64_t* out_a, uint64_t* out_b, u
     red_cnt = n + 1;
   } else if (mode == MODE_EDGE) {
     if (m) {
-      k_edge_gather<<<grid_for(m, g->sms), 256, 0, s>>>(g->acc.as<uint64_t>(), g->where.as<uint2>(), m,
-                                                         g->be.as<uint64_t>());
+      k_edge_gather<<<grid_for(m, g->sms), 256, 0, s>>>(g->acc.as<uint64_t>(), g->eid.as<uint32_t>(),
+                                                         g->nbr.as<uint32_t>(), g->pos.as<uint32_t>(),
+                                                         g->off.as<uint32_t>(), m, g->be.as<uint64_t>());
       KERNEL_CHECK(g);
     }
     CUDA_TRY(cudaMemcpyAsync(g->be.as<uint64_t>() + m, dtot, 8, cudaMemcpyDeviceToDevice, s));

@@ -155,10 +155,22 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_upsweep(const K* __restrict__
 struct RadixDecode {
   uint32_t* nbr;    // nbr[p] = nbr_last - (key & low B bits)
   uint32_t* src;    // src[p] = src_base + (key >> B)
-  uint32_t* where;  // where[slot id] = pos_base + p
-  uint32_t* vals;   // vals[p] = slot id
+  uint32_t* eid;    // U half: eid[p] = input edge id of the slot at p
+  uint32_t* pos;    // V half: twin positions (see below); global CSR positions
+  const uint32_t* off;
   uint64_t nbr_last, src_base, pos_base;
   int B, Be, side;
+  // U half: also write the V half's input, transposed and reversed -- record
+  // m-1-p holds the twin slot (nbr -> src) keyed ((nbr - tbase) << tB | (tbase
+  // - 1 - src)) with the U position p as payload ([<< Be | p] or value p), so a
+  // stable sort on its high field alone orders the V half (the low field is
+  // already descending src).  The V half's last pass then knows both twins'
+  // positions p and q: pos[q] = p - off[u] (index of v in N(u)) and pos[p] =
+  // q - off[v] (index of u in N(v)) -- Alg. 1's twin indices with no search.
+  uint64_t* tkeys;
+  uint32_t* tvals;
+  uint64_t tm, tbase;
+  int tB;
 };
 
 #ifndef BF_RS_MINB
@@ -240,11 +252,25 @@ __global__ void __launch_bounds__(RS_THREADS, BF_RS_MINB) k_rs_downsweep(const K
       const uint32_t d = (uint32_t)(kr >> shift) & mask;
       const size_t gp = (uint32_t)(goff[d] + i);
       const uint64_t k = kr >> dec.Be;
-      const uint32_t slot = VALS ? svals[i] : (uint32_t)(2 * (kr & emask) + dec.side);
-      dec.nbr[gp] = (uint32_t)(dec.nbr_last - (k & lmask));
-      dec.src[gp] = (uint32_t)(dec.src_base + (k >> dec.B));
-      dec.vals[gp] = slot;
-      dec.where[slot] = (uint32_t)(dec.pos_base + gp);
+      const uint32_t payload = VALS ? svals[i] : (uint32_t)(kr & emask);  // U: edge id; V: U position
+      const uint32_t nb = (uint32_t)(dec.nbr_last - (k & lmask)), sr = (uint32_t)(dec.src_base + (k >> dec.B));
+      dec.nbr[gp] = nb;
+      dec.src[gp] = sr;
+      if (dec.tkeys) {  // U half
+        dec.eid[gp] = payload;
+        const uint64_t tk = ((uint64_t)(nb - dec.tbase) << dec.tB) | (dec.tbase - 1 - sr);
+        const size_t tp = dec.tm - 1 - gp;
+        if (VALS) {
+          dec.tkeys[tp] = tk;
+          dec.tvals[tp] = (uint32_t)gp;
+        } else {
+          dec.tkeys[tp] = (tk << dec.Be) | gp;
+        }
+      } else {  // V half: q = pos_base + gp, twin at U position payload
+        const uint32_t q = (uint32_t)(dec.pos_base + gp);
+        dec.pos[q] = payload - __ldg(dec.off + nb);
+        dec.pos[payload] = q - __ldg(dec.off + sr);
+      }
     }
     return;
   }
@@ -271,10 +297,9 @@ int radix_impl(K* k0, uint32_t* v0, K* k1, uint32_t* v1, size_t n, int begin_bit
   K* ki = k0; K* ko = k1;
   uint32_t* vi = v0; uint32_t* vo = v1;
   int which = 0;
-  const RadixDecode none = {nullptr, nullptr, nullptr, nullptr, 0, 0, 0, 0, 0, 0};
+  const RadixDecode none = {nullptr, nullptr, nullptr, nullptr, nullptr, 0, 0, 0, 0, 0, 0, nullptr, nullptr, 0, 0, 0};
   for (int p = 0, sh = begin_bit; p < passes; p++, sh += bits) {
     RadixDecode d = (dec && p == passes - 1) ? *dec : none;
-    if (d.nbr && !d.vals) d.vals = vo;  // (key, value) records: slot ids to the pass's value output
     k_rs_upsweep<K><<<ntiles, RS_THREADS, 0, s>>>(ki, n, sh, bits, counts, ntiles);
     (*launches)++;
     CUDA_TRY(cudaGetLastError());
@@ -318,14 +343,18 @@ int radix_sort_u64(uint64_t* k0, uint32_t* v0, uint64_t* k1, uint32_t* v1, size_
                    void* temp, cudaStream_t s, uint64_t* launches) {
   return radix_impl<uint64_t>(k0, v0, k1, v1, n, begin_bit, end_bit, temp, s, launches);
 }
-int radix_sort_slots(uint64_t* k0, uint32_t* v0, uint64_t* k1, uint32_t* v1, size_t n, int key_bits, int B, int Be,
-                     int side, uint64_t nbr_last, uint64_t src_base, uint64_t pos_base, uint32_t* nbr, uint32_t* src,
-                     uint32_t* where, void* temp, cudaStream_t s, uint64_t* launches) {
-  RadixDecode dec = {nbr, src, where, nullptr, nbr_last, src_base, pos_base, B, Be, side};
-  if (Be) {  // packed records: slot ids to v0
-    dec.vals = v0;
-    radix_impl<uint64_t>(k0, nullptr, k1, nullptr, n, Be, Be + key_bits, temp, s, launches, &dec);
-    return 0;
+void radix_sort_slots(uint64_t* k0, uint32_t* v0, uint64_t* k1, uint32_t* v1, size_t n, int key_bits, int skip_bits,
+                      int B, int Be, uint64_t nbr_last, uint64_t src_base, uint64_t pos_base, uint32_t* nbr,
+                      uint32_t* src, uint32_t* eid, uint32_t* pos, const uint32_t* off, const SlotTranspose* tr,
+                      void* temp, cudaStream_t s, uint64_t* launches) {
+  RadixDecode dec = {nbr, src, eid, pos, off, nbr_last, src_base, pos_base, B, Be, tr ? 0 : 1, nullptr, nullptr, 0, 0, 0};
+  if (tr) {
+    dec.tkeys = tr->keys;
+    dec.tvals = tr->vals;
+    dec.tm = n;
+    dec.tbase = tr->base;
+    dec.tB = tr->B;
   }
-  return radix_impl<uint64_t>(k0, v0, k1, v1, n, 0, key_bits, temp, s, launches, &dec);
+  if (Be) radix_impl<uint64_t>(k0, nullptr, k1, nullptr, n, Be + skip_bits, Be + key_bits, temp, s, launches, &dec);
+  else radix_impl<uint64_t>(k0, v0, k1, v1, n, skip_bits, key_bits, temp, s, launches, &dec);
 }

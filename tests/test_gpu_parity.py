@@ -94,7 +94,9 @@ def test_random_small(bf, seed):
 @pytest.mark.parametrize("flags", ["warp", "cta", "dense", "small_window", "dense+small_window", "light8",
                                    "small_chunk", "dense+small_chunk", "dense+small_window+small_chunk",
                                    "cta+small_window", "small_chunk+small_window", "dense+no_split+small_chunk",
-                                   "unpacked_sort"])
+                                   "unpacked_sort", "no_dense_row", "dense+no_dense_row",
+                                   "small_chunk+no_dense_row", "dense+small_chunk+no_dense_row", "key_buffer",
+                                   "dense+key_buffer", "dense+small_chunk+key_buffer"])
 @pytest.mark.parametrize("orient", ORIENTS)
 def test_forced_paths(bf, flags, orient):
     """T3: every start through one tier; tiny windows force the overflow paths
@@ -114,6 +116,10 @@ def test_forced_paths(bf, flags, orient):
         f |= bf.BF_FLAG_SMALL_CHUNK  # also drops the split threshold: giant-start pieces
     if "no_split" in flags:
         f |= bf.BF_FLAG_NO_SPLIT
+    if "key_buffer" in flags:
+        f |= bf.BF_FLAG_KEY_BUFFER  # slot-mode walks keep their keys for pass 2
+    if "no_dense_row" in flags:
+        f |= bf.BF_FLAG_NO_DENSE_ROW  # heavy tier: 4096-key window + global overflow rows
     if "unpacked_sort" in flags:
         f |= bf.BF_FLAG_UNPACKED_SORT  # the c5-size slot sort (key and value arrays)
     opts = dict(test_flags=f)
@@ -334,7 +340,8 @@ def test_random_graphs_random_paths(bf, seed):
     m = int(min(n_u * n_v // 3, rng.integers(200, 25000)))
     g = bfgen.chung_lu(n_u, n_v, m, float(rng.uniform(1.8, 2.6)), float(rng.uniform(1.8, 2.6)), seed=seed + 1)
     ref = oracle.count(g.n_u, g.n_v, g.edges)
-    names = ["FORCE_WARP", "FORCE_CTA", "FORCE_DENSE", "SMALL_WINDOW", "SMALL_CHUNK", "NO_SPLIT", "UNPACKED_SORT"]
+    names = ["FORCE_WARP", "FORCE_CTA", "FORCE_DENSE", "SMALL_WINDOW", "SMALL_CHUNK", "NO_SPLIT", "UNPACKED_SORT",
+             "NO_DENSE_ROW", "KEY_BUFFER"]
     f = 0
     for nm in names:
         if rng.random() < 0.3:
