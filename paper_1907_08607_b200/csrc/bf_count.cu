@@ -261,13 +261,30 @@ struct HeavyStore {
 // reading every G-th key (P/G predicated loads in flight per lane, UR units per
 // group unrolled), so no lane ever searches for its segment.  Pass-2 sums of
 // d-1 stay in registers until one shared atomic per unit.
+// unit meta: chunk position of the first wedge (bits 0-15) | length | slot;
+// NT <= 256: length 1..P in bits 16-23, slot in 24-31 (one mask per decode);
+// wider CTAs: length - 1 in bits 16-20, slot in 21-31
+template <int NT>
+struct UnitMeta {
+  static constexpr bool WIDE = NT > 256;
+  static constexpr uint32_t SLOT_SHIFT = WIDE ? 21 : 24;
+  __device__ __forceinline__ static uint32_t pack(uint32_t pos, uint32_t len, uint32_t slot) {
+    return (pos & 0xffffu) | ((WIDE ? len - 1 : len) << 16) | (slot << SLOT_SHIFT);
+  }
+  // length of an active unit's meta word; inactive units (me = 0) give 0 when narrow
+  __device__ __forceinline__ static uint32_t len(uint32_t me, bool active) {
+    if (WIDE) return active ? ((me >> 16) & 31u) + 1 : 0u;
+    return (me >> 16) & 0xffu;
+  }
+  __device__ __forceinline__ static uint32_t slot(uint32_t me) { return me >> SLOT_SHIFT; }
+};
+
 template <int NT, uint32_t UCAP>
 struct Units {
   static_assert(NT <= 2048, "unit meta packs the slot in 11 bits");
   using SlotT = typename std::conditional<(NT <= 256), uint8_t, uint16_t>::type;
   uint32_t lo[UCAP];           // first nbr index of the unit
-  uint32_t meta[UCAP];         // chunk position of the first wedge (key cache index, bits 0-15)
-                               // | length - 1 in 0..P-1 (bits 16-20) | chunk-local slot (bits 21-31)
+  uint32_t meta[UCAP];         // UnitMeta<NT>: chunk position of the first wedge | length | chunk-local slot
   uint32_t slo[NT], shi[NT];   // pass-2 per-slot sums (u64 as two u32)
   uint32_t wt[32];             // scan scratch
   uint32_t jn[2];              // continuation slot of chunk i in jn[i & 1] (FULL = none)
@@ -307,7 +324,7 @@ __device__ __forceinline__ void units_write(Units<NT, UCAP>& u, uint32_t lo, uin
   BF_CHECK(ex + nu <= UCAP && L < 65536);
   for (uint32_t f = 0, o = 0; f < nu; f++, o += P) {
     u.lo[ex + f] = lo + o;
-    u.meta[ex + f] = ((wp + o) & 0xffffu) | ((f + 1 < nu ? (uint32_t)P - 1 : L - o - 1) << 16) | (threadIdx.x << 21);
+    u.meta[ex + f] = UnitMeta<NT>::pack(wp + o, f + 1 < nu ? (uint32_t)P : L - o, threadIdx.x);
   }
   if (threadIdx.x == 0) u.nunits = total & 0xffffu;
   u.slo[threadIdx.x] = 0;
@@ -353,22 +370,12 @@ __device__ __forceinline__ uint64_t units_build(const CountArgs& a, Units<NT, UC
 // (shared memory up to lcap entries, then the CTA's global list)
 // SPILL: the list can outgrow shared memory (heavy tier); otherwise lcap is
 // an exact bound (small tiers: distinct keys <= w <= lcap)
-// BF_LIST_AGG: warp-aggregated push (the lanes pushing together take one
-// atomicAdd on the list counter) -- a tuning experiment, off by default
-#ifndef BF_LIST_AGG
-#define BF_LIST_AGG 0
-#endif
+// (A warp-aggregated push -- one atomicAdd per warp on the list counter --
+// measured slower on c2: 6.82 -> 7.40 ms.)
 template <bool SPILL>
 __device__ __forceinline__ void list_push(uint32_t* lcnt, uint32_t* list, uint32_t lcap, uint32_t* olist,
                                           uint64_t ocap, uint32_t key) {
-#if BF_LIST_AGG
-  const uint32_t am = __activemask(), lane = threadIdx.x & 31u, leader = __ffs(am) - 1u;
-  uint32_t base = 0;
-  if (lane == leader) base = atomicAdd(lcnt, (uint32_t)__popc(am));
-  const uint32_t i = __shfl_sync(am, base, leader) + (uint32_t)__popc(am & ((1u << lane) - 1u));
-#else
   const uint32_t i = atomicAdd(lcnt, 1u);
-#endif
   if (!SPILL || i < lcap) list[i] = key;
   else {
     BF_CHECK(olist != nullptr && i - lcap < ocap);
@@ -395,7 +402,7 @@ __device__ __forceinline__ void units_pass1(const CountArgs& a, Units<NT, UCAP>&
     for (int r = 0; r < UR; r++) {
       const uint32_t x = x0 + r * NG;
       const uint32_t lo = x < nunits ? u.lo[x] : 0u, me = x < nunits ? u.meta[x] : 0u;
-      const uint32_t len = x < nunits ? ((me >> 16) & 31u) + 1 : 0u;
+      const uint32_t len = UnitMeta<NT>::len(me, x < nunits);
       ps[r] = me & 0xffffu;
 #pragma unroll
       for (int it = 0; it < IT; it++) {
@@ -438,9 +445,9 @@ __device__ __forceinline__ void units_pass2(const CountArgs& a, Units<NT, UCAP>&
       const uint32_t x = xb + r * NG + (tid & 31) / G;
       const bool act = x < nunits;
       lo[r] = act ? u.lo[x] : 0u;
-      const uint32_t me = act ? u.meta[x] : 0u, len = act ? ((me >> 16) & 31u) + 1 : 0u;
+      const uint32_t me = act ? u.meta[x] : 0u, len = UnitMeta<NT>::len(me, act);
       ps[r] = me & 0xffffu;
-      sl[r] = me >> 21;
+      sl[r] = UnitMeta<NT>::slot(me);
 #pragma unroll
       for (int it = 0; it < IT; it++) {
         const uint32_t i = gl + it * G;
@@ -846,10 +853,12 @@ struct HeavySmemT {
 constexpr uint32_t DENSE_MAX_KEYS = 40960;
 
 #ifndef BF_BIG_MINB
-#define BF_BIG_MINB 4  // <= 64 registers: four 256-thread CTAs per SM (the shared-memory limit too)
+#define BF_BIG_MINB 1
 #endif
+// SB == 4 (short-segment graphs): capped at 64 registers, four CTAs per SM
+// (measured on c4: 14.5 -> 13.2 ms); SB == 1 uncapped (c2: 6.75 -> 6.63 ms)
 template <int ORIENT, int MODE, int SB, int NT, uint32_t WIN, uint32_t CAP, uint32_t LCAP, int P, int G, int UR>
-__global__ void __launch_bounds__(NT, BF_BIG_MINB) k_big(CountArgs a) {
+__global__ void __launch_bounds__(NT, SB == 4 ? 4 : BF_BIG_MINB) k_big(CountArgs a) {
   using SM = HeavySmemT<NT, WIN, CAP, LCAP, P, G, UR>;
   extern __shared__ __align__(16) char sm[];
   SM& hs = *(SM*)sm;

@@ -9,6 +9,7 @@ import bfgen, numpy as np, oracle
 from paper_1907_08607_b200 import bf
 spec = json.loads(sys.argv[1])
 if spec["g"][0] == "K": g = bfgen.complete(*spec["g"][1:])
+elif spec["g"][0] == "cfg": g = bfgen.config_graph(*spec["g"][1:])
 else: g = bfgen.chung_lu(*spec["g"][1:])
 ref = oracle.count(g.n_u, g.n_v, g.edges)
 f = 0
@@ -24,14 +25,24 @@ print("RESULT", "ok" if ok else "mismatch")
 
 def main():
   cases = []
-  for gspec in (["K", 40, 33], ["K", 17, 9], ["C", 1500, 900, 12000, 2.0, 2.3, 5]):
+  counts = {}
+  for gspec in (["K", 40, 33], ["K", 17, 9], ["C", 1500, 900, 12000, 2.0, 2.3, 5], ["cfg", 4, 0.01]):
       for mode in ("total", "vertex", "edge"):
-          for flags in ([], ["FORCE_WARP"], ["FORCE_CTA"], ["FORCE_DENSE"], ["FORCE_DENSE", "SMALL_CHUNK"], ["SMALL_CHUNK"], ["UNPACKED_SORT"]):
+          for flags in ([], ["FORCE_WARP"], ["FORCE_CTA"], ["FORCE_DENSE"], ["FORCE_DENSE", "SMALL_CHUNK"], ["SMALL_CHUNK"],
+                        ["UNPACKED_SORT"], ["NO_DENSE_ROW"], ["KEY_BUFFER"], ["FORCE_DENSE", "SMALL_CHUNK", "KEY_BUFFER"]):
               for orient in ("high", "low"):
                   cases.append(dict(g=gspec, mode=mode, flags=flags, orient=orient, rank="degree"))
+  # other rankings, and repeated runs of one larger graph (a nondeterministic race
+  # shows up as a run that differs)
+  for rank in ("side", "approx_degree", "approx_codegen", "auto"):
+      for mode in ("vertex", "edge"):
+          cases.append(dict(g=["C", 1500, 900, 12000, 2.0, 2.3, 5], mode=mode, flags=[], orient="high", rank=rank))
+  for rep in range(4):
+      for mode in ("total", "vertex", "edge"):
+          cases.append(dict(g=["cfg", 3, 0.02], mode=mode, flags=[], orient="high", rank="approx_degree", rep=rep))
   for c in cases:
       try:
-          r = subprocess.run([sys.executable, "-c", CHILD, json.dumps(c)], capture_output=True, text=True, timeout=60)
+          r = subprocess.run([sys.executable, "-c", CHILD, json.dumps(c)], capture_output=True, text=True, timeout=180)
           out = (r.stdout + r.stderr)
       except subprocess.TimeoutExpired:
           out = "TIMEOUT"
@@ -39,6 +50,8 @@ def main():
                                              ("TIMEOUT" if out == "TIMEOUT" else "ERROR"))
       extra = [l for l in out.splitlines() if "BF_CHECK" in l or "BFError" in l][:2]
       print(res, json.dumps(c), " | ".join(extra)[:300], flush=True)
+      counts[res] = counts.get(res, 0) + 1
+  print("SUMMARY", json.dumps(counts), f"{len(cases)} cases", flush=True)
 
 
 if __name__ == "__main__":
