@@ -181,30 +181,41 @@ __device__ __forceinline__ uint64_t* endpoint_slot(const CountArgs& a, uint32_t 
 __device__ __forceinline__ uint32_t hslot(uint32_t key, uint32_t shift) { return (key * 0x9E3779B1u) >> shift; }
 
 struct SmallStore {
-  uint32_t* win;  // u8 counters, four per word (key kk: byte kk)
+  uint32_t* win;  // u8 counters, four per word: bytes [0, WIN) the dense window (key kk: byte kk),
+                  // bytes [WIN, WIN + HS) the hash slots' counts (slot h: byte WIN + h)
   uint32_t* hk;
-  uint32_t* hv;   // u8 counts, four per word
-  uint32_t wl, hmask, shift;
+  uint32_t* hv;   // = the hash counts (bytes WIN..), as words
+  uint32_t wl, hmask, shift, winb;
 
   // returns true if this increment took the key's count from 0 to 1
   __device__ __forceinline__ bool add(uint32_t key, uint32_t kk, bool& hashed) const {
+    uint32_t ci;
+    return add_ci(key, kk, hashed, ci);
+  }
+  // the same, and the counter's byte index ci (window: kk; hash slot h: WIN + h)
+  __device__ __forceinline__ bool add_ci(uint32_t key, uint32_t kk, bool& hashed, uint32_t& ci) const {
     if (__builtin_expect(kk < wl, 1)) {
-      BF_CHECK(__isShared(win + (kk >> 2)));
-      const uint32_t sh = (kk & 3u) << 3;
-      const uint32_t old = atomicAdd(win + (kk >> 2), 1u << sh);
-      return ((old >> sh) & 0xffu) == 0u;
-    }
-    hashed = true;
-    uint32_t h = hslot(key, shift);
-    for (uint32_t probes = 0;; probes++) {
-      if (probes > hmask) __trap();  // more distinct keys than slots: impossible by the tier bound
-      const uint32_t cur = atomicCAS(hk + h, EMPTY, key);
-      if (cur == EMPTY || cur == key) {
-        const uint32_t sh = (h & 3u) << 3;
-        return ((atomicAdd(hv + (h >> 2), 1u << sh) >> sh) & 0xffu) == 0u;
+      ci = kk;
+    } else {
+      hashed = true;
+      uint32_t h = hslot(key, shift);
+      for (uint32_t probes = 0;; probes++) {
+        if (probes > hmask) __trap();  // more distinct keys than slots: impossible by the tier bound
+        const uint32_t cur = atomicCAS(hk + h, EMPTY, key);
+        if (cur == EMPTY || cur == key) break;
+        h = (h + 1) & hmask;
       }
-      h = (h + 1) & hmask;
+      ci = winb + h;
     }
+    BF_CHECK(__isShared(win + (ci >> 2)));
+    const uint32_t sh = (ci & 3u) << 3;
+    const uint32_t old = atomicAdd(win + (ci >> 2), 1u << sh);
+    return ((old >> sh) & 0xffu) == 0u;
+  }
+  __device__ __forceinline__ uint32_t at(uint32_t ci) const { return ((const uint8_t*)win)[ci]; }
+  __device__ __forceinline__ void zero_at(uint32_t ci) const {
+    ((uint8_t*)win)[ci] = 0;
+    if (ci >= winb) hk[ci - winb] = EMPTY;
   }
   __device__ __forceinline__ uint32_t get(uint32_t key, uint32_t kk) const {
     if (__builtin_expect(kk < wl, 1)) return ((const uint8_t*)win)[kk];
@@ -213,7 +224,7 @@ struct SmallStore {
       if (probes > hmask) __trap();  // the key was inserted in pass 1
       h = (h + 1) & hmask;
     }
-    return ((const uint8_t*)hv)[h];
+    return ((const uint8_t*)win)[winb + h];
   }
   // reset one key (every key of the start is reset, so deleting hash entries
   // never strands a lookup: get() probes past EMPTY slots)
@@ -225,7 +236,7 @@ struct SmallStore {
     uint32_t h = hslot(key, shift);
     while (hk[h] != key) h = (h + 1) & hmask;
     hk[h] = EMPTY;
-    ((uint8_t*)hv)[h] = 0;
+    ((uint8_t*)win)[winb + h] = 0;
   }
 };
 
@@ -374,8 +385,9 @@ __device__ __forceinline__ uint64_t units_build(const CountArgs& a, Units<NT, UC
 // measured slower on c2: 6.82 -> 7.40 ms.)
 template <bool SPILL>
 __device__ __forceinline__ void list_push(uint32_t* lcnt, uint32_t* list, uint32_t lcap, uint32_t* olist,
-                                          uint64_t ocap, uint32_t key) {
+                                          uint64_t ocap, uint32_t key, uint16_t* listi = nullptr, uint32_t ci = 0) {
   const uint32_t i = atomicAdd(lcnt, 1u);
+  if (listi) listi[i] = (uint16_t)ci;  // small tiers: the owner's counter index
   if (!SPILL || i < lcap) list[i] = key;
   else {
     BF_CHECK(olist != nullptr && i - lcap < ocap);
@@ -388,10 +400,13 @@ __device__ __forceinline__ uint32_t list_get(const uint32_t* list, uint32_t lcap
 }
 
 // pass 1 over the chunk's units: d(key) += 1 per wedge
+// CACHE (small tiers): each wedge's counter index goes to cache[chunk position]
+// and each owner's to listi, so pass 2, finalize and the reset read counters
+// directly -- no key reload, window test or hash probe after pass 1
 template <bool SPILL, bool CACHE, int NT, int P, int G, int UR, uint32_t UCAP, class Store>
 __device__ __forceinline__ void units_pass1(const CountArgs& a, Units<NT, UCAP>& u, const Store& cs,
                                             uint32_t kbase, uint32_t* list, uint32_t lcap, uint32_t* olist,
-                                            bool& hashed, uint32_t* cache) {
+                                            bool& hashed, uint16_t* cache, uint16_t* listi) {
   constexpr int IT = P / G;
   constexpr uint32_t NG = NT / G;
   const uint32_t tid = threadIdx.x, gl = tid & (G - 1);
@@ -418,8 +433,14 @@ __device__ __forceinline__ void units_pass1(const CountArgs& a, Units<NT, UCAP>&
         uint32_t k = key[r][it];
         if (k != EMPTY) {
           BF_CHECK(k < a.n);
-          if (CACHE) cache[ps[r] + gl + it * G] = k;
-          if (cs.add(k, k - kbase, hashed)) list_push<SPILL>(&u.lcnt, list, lcap, olist, a.olist_len, k);
+          if constexpr (CACHE) {
+            uint32_t ci;
+            const bool first = cs.add_ci(k, k - kbase, hashed, ci);
+            cache[ps[r] + gl + it * G] = (uint16_t)ci;
+            if (first) list_push<SPILL>(&u.lcnt, list, lcap, olist, a.olist_len, k, listi, ci);
+          } else {
+            if (cs.add(k, k - kbase, hashed)) list_push<SPILL>(&u.lcnt, list, lcap, olist, a.olist_len, k);
+          }
         }
       }
   }
@@ -432,7 +453,7 @@ __device__ __forceinline__ void units_pass1(const CountArgs& a, Units<NT, UCAP>&
 // d-1 fits u32 and the group reduction shuffles 32-bit words
 template <int MODE, bool CACHE, int NT, int P, int G, int UR, uint32_t UCAP, class Store, bool NARROW = true>
 __device__ __forceinline__ void units_pass2(const CountArgs& a, Units<NT, UCAP>& u, const Store& cs,
-                                            uint32_t kbase, const uint32_t* cache) {
+                                            uint32_t kbase, const uint16_t* cache) {
   constexpr int IT = P / G;
   constexpr uint32_t NG = NT / G;
   const uint32_t tid = threadIdx.x, gl = tid & (G - 1);
@@ -451,7 +472,8 @@ __device__ __forceinline__ void units_pass2(const CountArgs& a, Units<NT, UCAP>&
 #pragma unroll
       for (int it = 0; it < IT; it++) {
         const uint32_t i = gl + it * G;
-        key[r][it] = i < len ? (CACHE ? cache[ps[r] + i] : __ldg(a.nbr + (lo[r] + i))) : EMPTY;
+        if constexpr (CACHE) key[r][it] = i < len ? (uint32_t)cache[ps[r] + i] : EMPTY;  // counter index
+        else key[r][it] = i < len ? __ldg(a.nbr + (lo[r] + i)) : EMPTY;
       }
     }
 #pragma unroll
@@ -461,7 +483,9 @@ __device__ __forceinline__ void units_pass2(const CountArgs& a, Units<NT, UCAP>&
 #pragma unroll
       for (int it = 0; it < IT; it++) {
         if (key[r][it] != EMPTY) {
-          const uint32_t c = cs.get(key[r][it], key[r][it] - kbase) - 1u;
+          uint32_t c;
+          if constexpr (CACHE) c = cs.at(key[r][it]) - 1u;
+          else c = cs.get(key[r][it], key[r][it] - kbase) - 1u;
           s += c;
           if (MODE == MODE_EDGE && c) red_add_u64(a.acc + (lo[r] + gl + it * G), c);  // edge (y, key)
         }
@@ -490,15 +514,20 @@ __device__ __forceinline__ void slot_flush(const CountArgs& a, const uint32_t* s
 template <int MODE, bool SPILL, int NT, class Store>
 __device__ __forceinline__ void list_finalize(const CountArgs& a, const Store& cs, uint32_t kbase, uint32_t cnt,
                                               const uint32_t* list, uint32_t lcap, const uint32_t* olist,
-                                              uint64_t& lsum) {
+                                              uint64_t& lsum, const uint16_t* listi = nullptr) {
   for (uint32_t i = threadIdx.x; i < cnt; i += NT) {
     const uint32_t key = list_get<SPILL>(list, lcap, olist, i), kk = key - kbase;
     BF_CHECK(key < a.n);
-    const uint32_t d = cs.get(key, kk);
+    uint32_t d;
+    if constexpr (SPILL) d = cs.get(key, kk);
+    else d = listi ? cs.at(listi[i]) : cs.get(key, kk);
     // small tiers reset here in total mode; the heavy tier resets after a barrier
     // (resetting inside this loop, next to other threads' reads of the global
     // overflow row, measured 4x slower on c3)
-    if (MODE == MODE_TOTAL && !SPILL) cs.zero(key, kk);
+    if constexpr (MODE == MODE_TOTAL && !SPILL) {
+      if (listi) cs.zero_at(listi[i]);
+      else cs.zero(key, kk);
+    }
     // small tiers: d <= 128, so C(d,2) in 32 bits
     const uint64_t c2 = SPILL ? choose2(d) : (uint64_t)((d * (d - (d > 0))) >> 1);
     lsum += c2;
@@ -523,11 +552,12 @@ __device__ __forceinline__ void start_passes(const CountArgs& a, Units<NT, UCAP>
                                              const Start& st, bool single, uint64_t base, uint64_t w, uint64_t K1,
                                              uint32_t cap, uint32_t jn0, bool mine, uint32_t myj, uint32_t myy,
                                              uint32_t* list, uint32_t lcap, uint32_t* olist, uint64_t& lsum,
-                                             uint64_t& pairs, bool& hashed, Prof& pf, uint32_t* cache) {
+                                             uint64_t& pairs, bool& hashed, Prof& pf, uint16_t* cache,
+                                             uint16_t* listi) {
   const uint32_t tid = threadIdx.x;
   // ---- pass 1 (first chunk already built)
-  if (single) units_pass1<SPILL, CACHE, NT, P, G, UR, UCAP>(a, u, cs, st.kbase, list, lcap, olist, hashed, cache);
-  else units_pass1<SPILL, false, NT, P, G, UR, UCAP>(a, u, cs, st.kbase, list, lcap, olist, hashed, nullptr);
+  if (single) units_pass1<SPILL, CACHE, NT, P, G, UR, UCAP>(a, u, cs, st.kbase, list, lcap, olist, hashed, cache, listi);
+  else units_pass1<SPILL, false, NT, P, G, UR, UCAP>(a, u, cs, st.kbase, list, lcap, olist, hashed, nullptr, nullptr);
   pf.mark(2);
   cta_sync<NT>();
   pf.mark(3);
@@ -538,7 +568,7 @@ __device__ __forceinline__ void start_passes(const CountArgs& a, Units<NT, UCAP>
     while (K0 < w) {
       const uint64_t Kn = units_build<MODE, NT, P, UCAP>(a, u, jc, st.j1, base, K0, cap, par, mine, myj, myy);
       const uint32_t jn = u.jn[par];
-      units_pass1<SPILL, false, NT, P, G, UR, UCAP>(a, u, cs, st.kbase, list, lcap, olist, hashed, nullptr);
+      units_pass1<SPILL, false, NT, P, G, UR, UCAP>(a, u, cs, st.kbase, list, lcap, olist, hashed, nullptr, nullptr);
       cta_sync<NT>();
       if (tid == 0) u.jn[par] = FULL;
       jc = jn != FULL ? jn : ((st.j1 - jc > (uint32_t)NT) ? jc + NT : st.j1);
@@ -548,7 +578,7 @@ __device__ __forceinline__ void start_passes(const CountArgs& a, Units<NT, UCAP>
   }
   pf.mark(1);
   const uint32_t cnt = u.lcnt;
-  list_finalize<MODE, SPILL, NT>(a, cs, st.kbase, cnt, list, lcap, olist, lsum);
+  list_finalize<MODE, SPILL, NT>(a, cs, st.kbase, cnt, list, lcap, olist, lsum, CACHE ? listi : nullptr);
   if (tid == 0) pairs += cnt;
   pf.mark(4);
   if (MODE == MODE_TOTAL && SPILL) {
@@ -589,8 +619,12 @@ __device__ __forceinline__ void start_passes(const CountArgs& a, Units<NT, UCAP>
       }
     }
     for (uint32_t i = tid; i < cnt; i += NT) {
-      const uint32_t key = list_get<SPILL>(list, lcap, olist, i);
-      cs.zero(key, key - st.kbase);
+      if constexpr (CACHE) {
+        cs.zero_at(listi[i]);
+      } else {
+        const uint32_t key = list_get<SPILL>(list, lcap, olist, i);
+        cs.zero(key, key - st.kbase);
+      }
     }
   }
   pf.mark(6);
@@ -725,12 +759,15 @@ __device__ __forceinline__ void slots_pass2(const CountArgs& a, const Store& cs,
   }
 }
 
-// key cache per small tier (warp tier: NT == 32)
+// counter-index cache per small tier (warp tier: NT == 32): pass 1 records each
+// wedge's counter byte index (u16) and each owner's, pass 2 / finalize / reset
+// read the counters through them.  (Round 1's cache of the 32-bit KEYS was
+// slower than re-reading them through L1: 6.96 -> 6.85 ms without it.)
 #ifndef BF_WARP_CACHE
-#define BF_WARP_CACHE 0  // measured: the warp tier is faster re-reading keys through L1 (6.96 -> 6.85 ms)
+#define BF_WARP_CACHE 1
 #endif
 #ifndef BF_MED_CACHE
-#define BF_MED_CACHE 0
+#define BF_MED_CACHE 1
 #endif
 #define SMALL_CACHE(NT) ((NT) == 32 ? (BF_WARP_CACHE != 0) : (BF_MED_CACHE != 0))
 
@@ -744,11 +781,12 @@ template <int NT, uint32_t WIN, uint32_t HS, uint32_t CAP, int P, int G, int UR>
 struct SmallSmem {
   static constexpr uint32_t UCAP = CAP / P + NT;
   Units<NT, UCAP> u;
-  uint32_t win[WIN / 4];
+  uint32_t win[WIN / 4 + HS / 4];  // u8 counters: the dense window, then the hash slots' counts
   uint32_t hk[HS];
-  uint32_t hv[HS / 4];
   uint32_t list[CAP];   // distinct keys <= w <= CAP
-  uint32_t cache[SMALL_CACHE(NT) ? CAP : 1];  // the start's keys in wedge order (pass 2 reads them here)
+  uint16_t listi[SMALL_CACHE(NT) ? CAP : 2];  // the owners' counter indices
+  uint16_t cache[SMALL_CACHE(NT) ? CAP : 2];  // each wedge's counter index, in chunk order
+  static_assert(WIN + HS <= 65536, "counter indices are u16");
 };
 
 struct SlotRegs {
@@ -779,12 +817,13 @@ __global__ void __launch_bounds__(NT, NT == 32 ? 1 : BF_MED_MINB) k_small(CountA
   SmallStore cs;
   cs.win = ss.win;
   cs.hk = ss.hk;
-  cs.hv = ss.hv;
+  cs.hv = ss.win + WIN / 4;
   cs.wl = min(a.win, WIN);
+  cs.winb = WIN;
   cs.hmask = HS - 1;
   cs.shift = __clz(HS) + 1;  // 32 - log2(HS)
-  for (uint32_t i = tid; i < WIN / 4; i += NT) ss.win[i] = 0;
-  for (uint32_t i = tid; i < HS; i += NT) { ss.hk[i] = EMPTY; if (i < HS / 4) ss.hv[i] = 0; }
+  for (uint32_t i = tid; i < WIN / 4 + HS / 4; i += NT) ss.win[i] = 0;
+  for (uint32_t i = tid; i < HS; i += NT) ss.hk[i] = EMPTY;
   if (tid == 0) ss.u.lcnt = 0;
   cta_sync<NT>();
   uint64_t tot_acc = 0, pair_acc = 0;
@@ -817,7 +856,7 @@ __global__ void __launch_bounds__(NT, NT == 32 ? 1 : BF_MED_MINB) k_small(CountA
     bool hashed = false;
     start_passes<ORIENT, MODE, false, SMALL_CACHE(NT), NT, P, G, UR, SM::UCAP>(a, ss.u, cs, st, true, 0, 0, 0, CAP, FULL, sr.len != 0,
                                                        st.j0 + tid, sr.y, ss.list, CAP, nullptr, lsum, pair_acc,
-                                                       hashed, pf, ss.cache);
+                                                       hashed, pf, ss.cache, ss.listi);
     tot_acc += lsum;
     if (MODE == MODE_VERTEX) {
       const uint64_t t = warp_sum(lsum);
@@ -911,7 +950,7 @@ __global__ void __launch_bounds__(NT, SB == 4 ? 4 : BF_BIG_MINB) k_big(CountArgs
       const uint32_t jn0 = hs.u.jn[0];
       start_passes<ORIENT, MODE, true, false, NT, P, G, UR, SM::UCAP>(a, hs.u, cs, st, single, base, w, K1, cap, jn0,
                                                                       mine, myj, myy, hs.list, LCAP, olist, lsum,
-                                                                      pair_acc, hashed, pf, (uint32_t*)nullptr);
+                                                                      pair_acc, hashed, pf, (uint16_t*)nullptr, nullptr);
     }
     tot_acc += lsum;
     if (MODE == MODE_VERTEX) {
@@ -1049,9 +1088,9 @@ __global__ void __launch_bounds__(NT, NT == SP_NT ? 3 : 1) k_split_walk(CountArg
       }
       else if (DENSE)
         units_pass1<false, false, NT, SP_P, SP_G, 1, SplitSmem::UCAP>(a, ss.u, s1d, kbase, ss.list, SP_WIN, nullptr,
-                                                                         hashed, nullptr);
+                                                                         hashed, nullptr, nullptr);
       else units_pass1<false, false, NT, SP_P, SP_G, 1, SplitSmem::UCAP>(a, ss.u, s1, kbase, ss.list, SP_WIN, nullptr, hashed,
-                                                              nullptr);
+                                                              nullptr, nullptr);
       __syncthreads();
       if (tid == 0) ss.u.jn[par] = FULL;
       if (PASS2) slot_flush<MODE>(a, ss.u.slo, ss.u.shi, mine, myj, myy);
