@@ -129,8 +129,11 @@ const char* bf_last_error(void) { return g_err; }
 void bf_graph_destroy(bf_graph* g) {
   if (!g) return;
   DeviceGuard dg(g->device);
+  // stream-ordered frees: the memory returns to the pool when the stream gets
+  // there, so a caller's stream needs no sync; a library-owned one is drained
+  // before it is destroyed
   g->for_each_buf([](DevBuf& b) { b.release(); });
-  if (g->stream) cudaStreamSynchronize(g->stream);
+  if (g->own_stream && g->stream) cudaStreamSynchronize(g->stream);
   for (auto& e : g->ev)
     if (e) cudaEventDestroy(e);
   if (g->own_stream && g->stream) cudaStreamDestroy(g->stream);

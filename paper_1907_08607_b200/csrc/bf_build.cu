@@ -406,6 +406,7 @@ __global__ void k_pieces(const uint4* __restrict__ split, const uint4* __restric
   }
 }
 
+
 __global__ void k_compact2(const uint32_t* __restrict__ flag, const uint32_t* __restrict__ idx,
                            const uint32_t* __restrict__ key, uint64_t n, uint32_t* __restrict__ out_rid,
                            uint32_t* __restrict__ out_key) {
@@ -676,13 +677,16 @@ bf_status graph_plan(bf_graph* g) {
   if (g->opt.test_flags & BF_FLAG_FORCE_WARP) tr.tm = tr.tl;
   g->t1 = (uint32_t)tr.tl;
   g->t2 = (uint32_t)tr.tm;
+  // starts with wedges, sorted by (tier, wedges desc).  (Sorting every vertex
+  // instead, to save this sync, cost c4 -- 30K starts among 20M vertices --
+  // 2.2 ms.)
   uint32_t* nzf = g->tmp_c.as<uint32_t>();
   uint32_t* key = g->tmp_d.as<uint32_t>();
   uint32_t* idx = (uint32_t*)g->tmp_a.p;
   uint32_t* k0 = (uint32_t*)g->tmp_a.p + n1 + 16;
   uint32_t* v0 = g->tmp_f.as<uint32_t>();  // src no longer needed
   uint32_t* k1 = g->tmp_c.as<uint32_t>();  // reused after compaction
-  uint32_t* cnts = (uint32_t*)(g->tmp_b.as<char>() + 64);  // [0]=nz [1]=tier 0 [2]=tier 1
+  uint32_t* cnts = (uint32_t*)(g->tmp_b.as<char>() + 64);  // [0]=nz [1]=tier 0 [2]=tier 1 [3]=max heavy key range
   g->order.ensure(n1 * 4);
   CUDA_TRY(cudaMemsetAsync(cnts, 0, 16, s));
   if (n) {
@@ -707,16 +711,15 @@ bf_status graph_plan(bf_graph* g) {
   g->n_tier[0] = hc[1];
   g->n_tier[1] = hc[2];
   g->n_tier[2] = nnz - hc[1] - hc[2];
-  g->heavy_keys = hc[3] + 1;  // key offsets of heavy starts are < this
-  int w = radix_sort_u32(k0, v0, k1, g->order.as<uint32_t>(), nnz, 0, 32, tmp, s, L);
-  if (!w && nnz) CUDA_TRY(cudaMemcpyAsync(g->order.p, v0, (size_t)nnz * 4, cudaMemcpyDeviceToDevice, s));
+  const int w = radix_sort_u32(k0, v0, k1, g->order.as<uint32_t>(), nnz, 0, 32, tmp, s, L);
+  const uint32_t* order = (w || !nnz) ? g->order.as<uint32_t>() : v0;
   g->items.ensure((size_t)std::max<uint32_t>(nnz, 1) * 16);
   if (nnz) {
-    k_items<<<grid_for(nnz, g->sms), TPB, 0, s>>>(g->order.as<uint32_t>(), nnz, g->off.as<uint32_t>(),
-                                                   g->hi.as<uint32_t>(), g->wstart.as<uint64_t>(), g->orient,
-                                                   g->items.as<uint4>());
+    k_items<<<grid_for(nnz, g->sms), TPB, 0, s>>>(order, nnz, g->off.as<uint32_t>(), g->hi.as<uint32_t>(),
+                                                   g->wstart.as<uint64_t>(), g->orient, g->items.as<uint4>());
     KERNEL_CHECK(g);
   }
+  g->heavy_keys = hc[3] + 1;  // key offsets of heavy starts are < this
   return plan_split(g);
 }
 
@@ -733,7 +736,8 @@ static bf_status plan_split(bf_graph* g) {
   if (g->opt.test_flags & BF_FLAG_NO_SPLIT) g->split_threshold = ~0ull;
   const uint32_t nh = std::min<uint32_t>(g->n_tier[0], kMaxSplit);
   if (!nh) return BF_OK;
-  std::vector<uint4> it(nh);
+  std::vector<uint4>& it = g->h_items;
+  it.resize(nh);
   CUDA_TRY(cudaMemcpyAsync(it.data(), g->items.p, (size_t)nh * 16, cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaStreamSynchronize(s));
   uint32_t ns = 0;
@@ -741,8 +745,11 @@ static bf_status plan_split(bf_graph* g) {
   if (!ns) return BF_OK;
   // key range of each split start (HIGH: same-side rids ranked above s; LOW:
   // ranked below), row offsets, pieces, memory-bounded batches
-  std::vector<uint64_t> off(ns);
-  std::vector<uint4> pdesc;
+  // host tables live in the graph: the async uploads below may still read them
+  std::vector<uint64_t>& off = g->h_split_off;
+  std::vector<uint4>& pdesc = g->h_pdesc;
+  off.assign(ns, 0);
+  pdesc.clear();
   const uint64_t piece = std::max<uint64_t>(g->split_threshold / 2, 1);
   const uint64_t budget = kSplitRowBudget / 8;  // keys: row + list, 4 B each
   g->split_batches.push_back({0, 0, 0, 0, 0});
@@ -785,6 +792,5 @@ static bf_status plan_split(bf_graph* g) {
     g->slist.ensure(maxkeys * 4);
     CUDA_TRY(cudaMemsetAsync(g->srow.p, 0, maxkeys * 4, s));
   }
-  CUDA_TRY(cudaStreamSynchronize(s));  // host vectors go out of scope
   return BF_OK;
 }

@@ -193,6 +193,9 @@ struct bf_graph {
   DevBuf split_off;  // u64 [n_split] row offset (keys) inside the batch's rows
   DevBuf split_cnt;  // u32 [n_split] touched-list counts
   DevBuf pieces;     // uint4 [n_pieces] {split index, slot begin, slot end, -}
+  std::vector<uint4> h_items;        // host copy of the first items (split planning)
+  std::vector<uint64_t> h_split_off;  // host split tables (sources of async uploads)
+  std::vector<uint4> h_pdesc;
   DevBuf srow;       // u32 dense d-rows of the largest batch (kept zero between calls)
   DevBuf slist;      // u32 touched lists (same layout as srow)
 
