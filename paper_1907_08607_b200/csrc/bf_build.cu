@@ -28,11 +28,18 @@ inline unsigned grid_for(size_t n, int sms) {
 // degree increments are aggregated over the lanes of a warp that hold the same
 // vertex (__match_any_sync): power-law hubs (c4's Zipf items) would otherwise
 // serialise thousands of atomics on one address
+#ifndef BF_DEG_MATCH
+#define BF_DEG_MATCH 1
+#endif
 __device__ __forceinline__ void add_degree(uint32_t* deg, uint32_t z, bool valid) {
+#if BF_DEG_MATCH
   const uint32_t act = __ballot_sync(0xffffffffu, valid);
   if (!valid) return;
   const uint32_t peers = __match_any_sync(act, z);  // gid < n <= 2^32: a 32-bit match
   if ((threadIdx.x & 31) == (uint32_t)(__ffs(peers) - 1)) atomicAdd(&deg[z], (uint32_t)__popc(peers));
+#else
+  if (valid) atomicAdd(&deg[z], 1u);
+#endif
 }
 
 // Degree counting privatises what it can: a side of at most HIST_MAX vertices

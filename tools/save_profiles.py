@@ -1,43 +1,88 @@
-"""Copy a measurement run (tools/gpu_measure.sh <tag>) from gpurun_out/ into
-profiles/: the bench line, the launch list (+ summary) and the ncu --set full
-summary of the wedge kernels with DRAM bytes per count call."""
-import json, os, shutil, sys
+"""Copy a measurement run from gpurun_out/ into profiles/: the bench line, the
+launch list (+ per-kernel summary) and the ncu --set full summary of the wedge
+kernels of one count call, with the per-count DRAM bytes, kernel time, L2 hit
+rate, issue activity, warp instructions per wedge and the SHA-256 of the CUDA
+sources the capture measured (bench.py reports the summary as this build's
+`roofline.traffic` only when that hash matches).
+
+  python tools/save_profiles.py <tag> <config> <mode> [--bench <json>] [--launches <csv>] [--ncu <rep>]
+"""
+import argparse
+import json
+import os
+import shutil
+import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, os.path.join(ROOT, "tools"))
-import ncu_summary  # noqa: E402
+sys.path.insert(0, ROOT)
 import launch_summary  # noqa: E402
+import ncu_summary  # noqa: E402
 
 UNITS = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+TUNITS = {"ns": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1.0, "msecond": 1.0, "nsecond": 1e-6, "s": 1e3}
 
 
-def main(tag, config=2, mode="vertex", orient="high"):
-    g = os.path.join(ROOT, "gpurun_out")
+def qty(s, table):
+    v, u = s.split()
+    return float(v) * table.get(u, 1.0)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("tag")
+    ap.add_argument("config", type=int)
+    ap.add_argument("mode")
+    ap.add_argument("--bench")
+    ap.add_argument("--launches")
+    ap.add_argument("--ncu")
+    ap.add_argument("--W", type=float, default=None)
+    ap.add_argument("--orient", default="high")
+    a = ap.parse_args()
     p = os.path.join(ROOT, "profiles")
-    shutil.copy(os.path.join(g, f"{tag}_bench.json"), os.path.join(p, f"{tag}_bench_c{config}_{mode}.json"))
-    shutil.copy(os.path.join(g, f"{tag}_launches.csv"), os.path.join(p, f"{tag}_launches_c{config}_{mode}.csv"))
-    with open(os.path.join(p, f"{tag}_launches_c{config}_{mode}.txt"), "w") as f:
-        f.write(launch_summary.summarise(os.path.join(g, f"{tag}_launches.csv")) + "\n")
-    res = ncu_summary.load(os.path.join(g, f"{tag}_full.ncu-rep"))
-    dram = 0.0
-    for r in res:
-        b = 0.0
-        for key in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
-            v, u = r[key].split()
-            b += float(v) * UNITS[u]
-        r["dram_bytes"] = b
-        dram += b
-    out = {"config": config, "mode": mode, "orient": orient, "round": tag,
-           "command": "ncu --set full --clock-control none --import-source on -k regex:k_(big|small) -s 3 -c 3 "
-                      "python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e",
-           "dram_bytes_per_launch": dram,
-           "note": "one bf_count call = one launch each of the tier kernels listed; dram bytes summed over them",
-           "kernels": res}
-    json.dump(out, open(os.path.join(p, f"{tag}_ncu_full_c{config}_{mode}.json"), "w"), indent=1)
-    print(f"dram bytes per count call {dram:.4g}")
-    for r in res:
-        print(r["kernel"][:70], r["gpu__time_duration.sum"], f'{r["dram_bytes"] / 1e6:.1f} MB', r["lts__t_sector_hit_rate.pct"])
+    base = f"{a.tag}_c{a.config}_{a.mode}"
+    W = a.W
+    if a.bench:
+        shutil.copy(a.bench, os.path.join(p, f"{base}_bench.json"))
+        try:
+            W = W or json.loads(open(a.bench).readline())["config"]["W"]
+        except Exception:
+            pass
+    if a.launches:
+        shutil.copy(a.launches, os.path.join(p, f"{base}_launches.csv"))
+        with open(os.path.join(p, f"{base}_launches.txt"), "w") as f:
+            f.write(launch_summary.summarise(a.launches) + "\n")
+    if a.ncu:
+        import bench  # the same source hash bench.py computes
+        res = ncu_summary.load(a.ncu)
+        dram = t_ms = inst = 0.0
+        issue, l2 = [], []
+        for r in res:
+            b = sum(qty(r[k], UNITS) for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+            r["dram_bytes"] = b
+            dram += b
+            t = qty(r["gpu__time_duration.sum"], TUNITS)
+            t_ms += t
+            inst += float(r["smsp__inst_executed.sum"].split()[0])
+            issue.append((t, float(r["smsp__issue_active.avg.pct_of_peak_sustained_active"].split()[0])))
+            l2.append((b, float(r["lts__t_sector_hit_rate.pct"].split()[0])))
+        wsum = lambda xs: sum(w * v for w, v in xs) / max(sum(w for w, _ in xs), 1e-30)
+        out = {"config": a.config, "mode": a.mode, "orient": a.orient, "round": a.tag,
+               "src_sha": bench.src_sha(),
+               "command": "tools/ncu_kernel.sh: ncu --set full --clock-control none --import-source on "
+                          "-k regex:<wedge kernels> (one count call) python bench.py --steps 1 --warmup 1",
+               "dram_bytes_per_launch": dram, "kernel_ms": t_ms,
+               "l2_hit_pct": wsum(l2), "issue_active_pct": wsum(issue),
+               "warp_inst_per_wedge": inst / W if W else None,
+               "limiter": "L1/shared-memory wavefronts, shared-atomic latency and issue (see per-kernel stalls); "
+                          "DRAM is not the binding unit",
+               "note": "one bf_count call = one launch each of the kernels listed; bytes, time and instructions "
+                       "summed over them (ncu serialises and flushes caches: shares matter, not absolutes)",
+               "kernels": res}
+        json.dump(out, open(os.path.join(p, f"{base}_ncu_full.json"), "w"), indent=1)
+        print(f"{base}: dram {dram / 1e9:.3f} GB, kernels {t_ms:.3f} ms, L2 hit {wsum(l2):.1f}%, "
+              f"issue {wsum(issue):.1f}%, warp-inst/wedge {out['warp_inst_per_wedge']}")
 
 
 if __name__ == "__main__":
-    main(sys.argv[1])
+    main()
