@@ -250,23 +250,15 @@ __global__ void k_auto_w(const uint32_t* __restrict__ deg, const uint32_t* __res
 
 // ---- a3 -----------------------------------------------------------------------
 // rids are side-major (U in [0, nU), V in [nU, n)), so the U-end slots fill
-// the first m CSR positions and the V-end slots the last m: two sorts of m
-// keys with side-local bits, (src asc, dst rid desc): U slot i at keys[i], V
-// slot i at keys[m + i].  With Be > 0 the edge id i sits in the low Be bits of
-// the same u64 (no value arrays); else vals hold the slot ids 2i / 2i+1.
-__global__ void k_slot_keys(const uint32_t* __restrict__ e, uint64_t m, uint32_t nU, uint64_t n, int Bu, int Bv,
-                            int Be, const uint32_t* __restrict__ rid_of_gid, uint64_t* __restrict__ keys,
-                            uint32_t* __restrict__ vals) {
+// the first m CSR positions and the V-end slots the last m.  The U half is one
+// sort of m keys (rid(u) << Bv) | (n-1 - rid(v)) -- (src asc, dst rid desc);
+// the V half's records are laid out by the U half's last pass (radix_sort_slots_u).
+__global__ void k_slot_keys(const uint32_t* __restrict__ e, uint64_t m, uint32_t nU, uint64_t n, int Bv,
+                            const uint32_t* __restrict__ rid_of_gid, uint64_t* __restrict__ keys) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
-    uint2 uv = reinterpret_cast<const uint2*>(e)[i];
-    uint64_t ru = rid_of_gid[uv.x], rv = rid_of_gid[(uint64_t)nU + uv.y];
-    const uint64_t ku = (ru << Bv) | (n - 1 - rv);                    // nbr_last = n-1
-    if (Be) {
-      keys[i] = (ku << Be) | i;
-    } else {
-      keys[i] = ku;
-      vals[i] = (uint32_t)i;
-    }
+    const uint2 uv = reinterpret_cast<const uint2*>(e)[i];
+    const uint64_t ru = rid_of_gid[uv.x], rv = rid_of_gid[(uint64_t)nU + uv.y];
+    keys[i] = (ru << Bv) | (n - 1 - rv);
   }
 }
 
@@ -349,6 +341,16 @@ struct TierRule {
   uint32_t nU;           // side boundary (key range of a start)
 };
 
+// 14-bit monotone code of a start's wedge count (a float-like exponent and 9
+// mantissa bits): the plan sorts by (tier, code desc) over 16 bits -- two
+// radix passes -- which keeps the largest-first (LPT) order up to 1/512
+__device__ __forceinline__ uint32_t wedge_code(uint64_t w) {
+  if (w < 512) return (uint32_t)w;
+  const uint32_t e = 63u - (uint32_t)__clzll(w);  // >= 9
+  const uint32_t c = ((e - 8u) << 9) | (uint32_t)((w >> (e - 9u)) & 0x1FFu);
+  return c < 0x3FFFu ? c : 0x3FFFu;
+}
+
 __global__ void k_order_keys(const uint64_t* __restrict__ wstart, const uint32_t* __restrict__ off,
                              const uint32_t* __restrict__ hi, int orient, uint64_t n, TierRule tr,
                              uint32_t* __restrict__ nz, uint32_t* __restrict__ key, uint32_t* __restrict__ cnts) {
@@ -365,8 +367,7 @@ __global__ void k_order_keys(const uint64_t* __restrict__ wstart, const uint32_t
     }
     if (r < n) {
       nz[r] = w > 0;
-      const uint32_t wc = (uint32_t)(w > 0x3FFFFFFFull ? 0x3FFFFFFFull : w);
-      key[r] = (tier << 30) | (0x3FFFFFFFu - wc);
+      key[r] = (tier << 14) | (0x3FFFu - wedge_code(w));
     }
     // key range of a heavy start: same-side rids ranked above it (HIGH) or
     // below it (LOW); the heavy tier's per-CTA rows are sized by the maximum
@@ -557,7 +558,6 @@ bf_status graph_rank(bf_graph* g, int kind) {
   g->wstart.ensure(n1 * 8);
   g->nbr.ensure(S1 * 4);
   g->pos.ensure(S1 * 4);
-  g->eid.ensure(std::max<uint64_t>(m, 1) * 4);
   // scratch
   size_t big = std::max<size_t>(S1, n1);
   g->tmp_a.ensure(big * 8 + 64);            // keys0 (u64)
@@ -611,28 +611,22 @@ bf_status graph_rank(bf_graph* g, int kind) {
   const int Bv = std::max(1, ceil_log2_u64(std::max<uint64_t>(g->n_v, 1)));
   uint64_t* k0 = g->tmp_a.as<uint64_t>();
   uint64_t* k1 = g->tmp_b.as<uint64_t>();
-  uint32_t* v0 = g->tmp_c.as<uint32_t>();
-  uint32_t* v1 = g->tmp_d.as<uint32_t>();
   g->dflag.ensure(16);
   CUDA_TRY(cudaMemsetAsync(g->dflag.p, 0, 4, s));
   if (m) {
-    const int Be0 = std::max(1, ceil_log2_u64(m));
-    const int Be = (Bu + Bv + Be0 <= 64 && !(g->opt.test_flags & BF_FLAG_UNPACKED_SORT)) ? Be0 : 0;  // pack when it fits
-    k_slot_keys<<<grid_for(m, g->sms), TPB, 0, s>>>(g->edges.as<uint32_t>(), m, g->n_u, n, Bu, Bv, Be,
-                                                     g->rid_of_gid.as<uint32_t>(), k0, v0);
+    const int Be = std::max(1, ceil_log2_u64(m));  // bits of a U position
+    k_slot_keys<<<grid_for(m, g->sms), TPB, 0, s>>>(g->edges.as<uint32_t>(), m, g->n_u, n, Bv,
+                                                     g->rid_of_gid.as<uint32_t>(), k0);
     KERNEL_CHECK(g);
     uint32_t* src = g->tmp_f.as<uint32_t>();
     uint32_t* nbr = g->nbr.as<uint32_t>();
-    // U half: nbr = (n-1) - low, src = high, sorted over all its bits; its last
-    // pass also lays out the V half's records transposed and reversed, already
-    // in descending-u order, so the V half sorts over its v field only (Bv bits
-    // instead of Bu + Bv) and its last pass writes both twins' pos (Alg. 1
-    // l.5-6).  V half: nbr = (nU-1) - low, src = nU + high.
-    const SlotTranspose tr = {k0 + m, v0 + m, g->n_u, Bu};
-    radix_sort_slots(k0, v0, k1, v1, m, Bu + Bv, 0, Bv, Be, n - 1, 0, 0, nbr, src, g->eid.as<uint32_t>(), nullptr,
-                     nullptr, &tr, tmp, s, L);
-    radix_sort_slots(k0 + m, v0 + m, k1 + m, v1 + m, m, Bu + Bv, Bu, Bu, Be, (uint64_t)g->n_u - 1, g->n_u, m,
-                     nbr + m, src + m, nullptr, g->pos.as<uint32_t>(), g->off.as<uint32_t>(), nullptr, tmp, s, L);
+    // U half over Bu + Bv bits; its last pass lays out the V half's records
+    // (v field, U position), already in descending-u order, so the V half sorts
+    // over its v field only and its last pass writes both twins' pos (Alg. 1
+    // l.5-6).  Every record is one u64 (Bu + Bv <= 64, Bv + Be <= 63).
+    radix_sort_slots_u(k0, k1, m, Bu, Bv, Be, n, nbr, src, k0 + m, g->n_u, tmp, s, L);
+    radix_sort_slots_v(k0 + m, k1 + m, m, Bv, Be, g->n_u, nbr + m, src + m, g->pos.as<uint32_t>(),
+                       g->off.as<uint32_t>(), src, tmp, s, L);
   }
   if (n) {
     k_hi<<<grid_for(n, g->sms), TPB, 0, s>>>(g->nbr.as<uint32_t>(), g->off.as<uint32_t>(), g->rkey.as<uint64_t>(), n,
@@ -718,7 +712,7 @@ bf_status graph_plan(bf_graph* g) {
   g->n_tier[0] = hc[1];
   g->n_tier[1] = hc[2];
   g->n_tier[2] = nnz - hc[1] - hc[2];
-  const int w = radix_sort_u32(k0, v0, k1, g->order.as<uint32_t>(), nnz, 0, 32, tmp, s, L);
+  const int w = radix_sort_u32(k0, v0, k1, g->order.as<uint32_t>(), nnz, 0, 16, tmp, s, L);
   const uint32_t* order = (w || !nnz) ? g->order.as<uint32_t>() : v0;
   g->items.ensure((size_t)std::max<uint32_t>(nnz, 1) * 16);
   if (nnz) {

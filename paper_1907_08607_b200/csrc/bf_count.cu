@@ -387,7 +387,10 @@ template <bool SPILL>
 __device__ __forceinline__ void list_push(uint32_t* lcnt, uint32_t* list, uint32_t lcap, uint32_t* olist,
                                           uint64_t ocap, uint32_t key, uint16_t* listi = nullptr, uint32_t ci = 0) {
   const uint32_t i = atomicAdd(lcnt, 1u);
-  if (listi) listi[i] = (uint16_t)ci;  // small tiers: the owner's counter index
+  if (listi) {  // small tiers: only the owner's counter index (the key is recoverable from it)
+    listi[i] = (uint16_t)ci;
+    return;
+  }
   if (!SPILL || i < lcap) list[i] = key;
   else {
     BF_CHECK(olist != nullptr && i - lcap < ocap);
@@ -516,11 +519,22 @@ __device__ __forceinline__ void list_finalize(const CountArgs& a, const Store& c
                                               const uint32_t* list, uint32_t lcap, const uint32_t* olist,
                                               uint64_t& lsum, const uint16_t* listi = nullptr) {
   for (uint32_t i = threadIdx.x; i < cnt; i += NT) {
-    const uint32_t key = list_get<SPILL>(list, lcap, olist, i), kk = key - kbase;
+    uint32_t key, kk, d;
+    if constexpr (SPILL) {
+      key = list_get<SPILL>(list, lcap, olist, i);
+      kk = key - kbase;
+      d = cs.get(key, kk);
+    } else if (listi) {  // counter index -> key: window byte kk = key - kbase, or the hash slot's key
+      const uint32_t ci = listi[i];
+      key = ci < cs.winb ? kbase + ci : cs.hk[ci - cs.winb];
+      kk = key - kbase;
+      d = cs.at(ci);
+    } else {
+      key = list_get<SPILL>(list, lcap, olist, i);
+      kk = key - kbase;
+      d = cs.get(key, kk);
+    }
     BF_CHECK(key < a.n);
-    uint32_t d;
-    if constexpr (SPILL) d = cs.get(key, kk);
-    else d = listi ? cs.at(listi[i]) : cs.get(key, kk);
     // small tiers reset here in total mode; the heavy tier resets after a barrier
     // (resetting inside this loop, next to other threads' reads of the global
     // overflow row, measured 4x slower on c3)
@@ -783,8 +797,8 @@ struct SmallSmem {
   Units<NT, UCAP> u;
   uint32_t win[WIN / 4 + HS / 4];  // u8 counters: the dense window, then the hash slots' counts
   uint32_t hk[HS];
-  uint32_t list[CAP];   // distinct keys <= w <= CAP
-  uint16_t listi[SMALL_CACHE(NT) ? CAP : 2];  // the owners' counter indices
+  uint32_t list[SMALL_CACHE(NT) ? 1 : CAP];   // distinct keys <= w <= CAP (without the index cache)
+  uint16_t listi[SMALL_CACHE(NT) ? CAP : 2];  // the owners' counter indices (with it)
   uint16_t cache[SMALL_CACHE(NT) ? CAP : 2];  // each wedge's counter index, in chunk order
   static_assert(WIN + HS <= 65536, "counter indices are u16");
 };
@@ -1277,13 +1291,25 @@ __global__ void k_unrename(const uint64_t* __restrict__ bv, const uint32_t* __re
   }
 }
 
-// be[e] = the sums of the edge's two slots: U-half position p and its twin
-// off[v] + pos[p] in v's row
-__global__ void k_edge_gather(const uint64_t* __restrict__ acc, const uint32_t* __restrict__ eid,
-                              const uint32_t* __restrict__ nbr, const uint32_t* __restrict__ pos,
-                              const uint32_t* __restrict__ off, uint64_t m, uint64_t* __restrict__ be) {
-  for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < m; p += (uint64_t)gridDim.x * blockDim.x)
-    be[eid[p]] = acc[p] + acc[(size_t)off[nbr[p]] + pos[p]];
+// be[e] = the sums of the edge's two slots: the U slot at p = off[ru] + the
+// index of rv in N(ru) (a binary search: rows are sorted by decreasing rid) and
+// its twin off[rv] + pos[p]
+__global__ void k_edge_gather(const uint64_t* __restrict__ acc, const uint32_t* __restrict__ edges,
+                              const uint32_t* __restrict__ rid_of_gid, const uint32_t* __restrict__ nbr,
+                              const uint32_t* __restrict__ pos, const uint32_t* __restrict__ off, uint32_t nU,
+                              uint64_t m, uint64_t* __restrict__ be) {
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m; e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint2 uv = reinterpret_cast<const uint2*>(edges)[e];
+    const uint32_t ru = rid_of_gid[uv.x], rv = rid_of_gid[(uint64_t)nU + uv.y];
+    uint32_t lo = off[ru], hi = off[ru + 1];  // first index with nbr <= rv
+    while (lo < hi) {
+      const uint32_t mid = lo + ((hi - lo) >> 1);
+      if (nbr[mid] > rv) lo = mid + 1;
+      else hi = mid;
+    }
+    BF_CHECK(nbr[lo] == rv);
+    be[e] = acc[lo] + acc[(size_t)off[rv] + pos[lo]];
+  }
 }
 
 inline unsigned grid_for(size_t n, int sms) {
@@ -1565,9 +1591,10 @@ bf_status graph_count(bf_graph* g, int mode, uint64_t* out_a, uint64_t* out_b, u
     red_cnt = n + 1;
   } else if (mode == MODE_EDGE) {
     if (m) {
-      k_edge_gather<<<grid_for(m, g->sms), 256, 0, s>>>(g->acc.as<uint64_t>(), g->eid.as<uint32_t>(),
-                                                         g->nbr.as<uint32_t>(), g->pos.as<uint32_t>(),
-                                                         g->off.as<uint32_t>(), m, g->be.as<uint64_t>());
+      k_edge_gather<<<grid_for(m, g->sms), 256, 0, s>>>(g->acc.as<uint64_t>(), g->edges.as<uint32_t>(),
+                                                         g->rid_of_gid.as<uint32_t>(), g->nbr.as<uint32_t>(),
+                                                         g->pos.as<uint32_t>(), g->off.as<uint32_t>(), g->n_u, m,
+                                                         g->be.as<uint64_t>());
       KERNEL_CHECK(g);
     }
     CUDA_TRY(cudaMemcpyAsync(g->be.as<uint64_t>() + m, dtot, 8, cudaMemcpyDeviceToDevice, s));

@@ -90,27 +90,19 @@ int radix_sort_u32(uint32_t* k0, uint32_t* v0, uint32_t* k1, uint32_t* v1, size_
                    int end_bit, void* temp, cudaStream_t s, uint64_t* launches);
 int radix_sort_u64(uint64_t* k0, uint32_t* v0, uint64_t* k1, uint32_t* v1, size_t n, int begin_bit,
                    int end_bit, void* temp, cudaStream_t s, uint64_t* launches);
-// The slot sort of Alg. 1, one half at a time (keys (src - src_base) << B |
-// (nbr_last - nbr), key_bits wide, either with u32 values (Be = 0) or packed
-// above a Be-bit payload); its last pass writes the decoded CSR range (nbr,
-// src; pointers already offset to the range) instead of keys.  skip_bits: the
-// low key bits are already in order, the sort runs over [skip_bits, key_bits)
-// only.  U half (tr != null, payload = input edge id): also eid[p] and, via tr,
-// the V half's input records -- transposed, reversed, payload = the U position
-// -- keyed (nbr - base) << B | (base - 1 - src), so the V half is a stable sort
-// of them with skip_bits = B.  V half (tr == null, payload = U position p):
-// writes the twin indices pos[q] = p - off[u] and pos[p] = q - off[v] (pos,
-// off global; q = pos_base + local position).
-struct SlotTranspose {
-  uint64_t* keys;
-  uint32_t* vals;
-  uint64_t base;
-  int B;
-};
-void radix_sort_slots(uint64_t* k0, uint32_t* v0, uint64_t* k1, uint32_t* v1, size_t n, int key_bits, int skip_bits,
-                      int B, int Be, uint64_t nbr_last, uint64_t src_base, uint64_t pos_base, uint32_t* nbr,
-                      uint32_t* src, uint32_t* eid, uint32_t* pos, const uint32_t* off, const SlotTranspose* tr,
-                      void* temp, cudaStream_t s, uint64_t* launches);
+// The slot sort of Alg. 1 (bf_prims.cu), one half at a time; every record is
+// one u64 key, the last pass writes the decoded CSR range instead of keys.
+// U half: keys (rid(src)) << Bv | (n-1 - rid(dst)) over Bu + Bv bits; writes
+// nbr, src (pointers at the range's start) and the V half's input records to
+// vrec: at m-1-p, (rid(dst) - nU) << Be | p for the slot at U position p.
+// V half: sorts those records on their v field alone (they arrive in
+// descending-u order); writes nbr, src (range-local) and the twin indices
+// pos[q] = p - off[u], pos[p] = q - off[v] (global; usrc = the U half's src).
+void radix_sort_slots_u(uint64_t* k0, uint64_t* k1, size_t m, int Bu, int Bv, int Be, uint64_t n, uint32_t* nbr,
+                        uint32_t* src, uint64_t* vrec, uint64_t nU, void* temp, cudaStream_t s, uint64_t* launches);
+void radix_sort_slots_v(uint64_t* k0, uint64_t* k1, size_t m, int Bv, int Be, uint64_t nU, uint32_t* nbr,
+                        uint32_t* src, uint32_t* pos, const uint32_t* off, const uint32_t* usrc, void* temp,
+                        cudaStream_t s, uint64_t* launches);
 
 static inline int ceil_log2_u64(uint64_t x) {  // bits needed to hold values < x (x>=1)
   int b = 0;
@@ -162,7 +154,6 @@ struct bf_graph {
   DevBuf nbr;         // u32 [2m]
   DevBuf pos;         // u32 [2m]  index of src in N(dst)
   DevBuf hi;          // u32 [n]   deg_x(x)
-  DevBuf eid;         // u32 [m]   input edge id of each U-half slot (the per-edge output gather)
   DevBuf wstart;      // u64 [n]   wedges per start rid (current orientation)
   DevBuf seglo;       // u32 [2m]  per slot (s->y): first index in nbr of its wedge segment
   DevBuf seglen;      // u32 [2m]  per slot: segment length (scratch of the plan)
@@ -219,7 +210,7 @@ struct bf_graph {
   uint64_t last_pairs = 0;  // distinct endpoint pairs (d >= 1) aggregated by the last count
 
   template <class F> void for_each_buf(F f) {
-    DevBuf* bufs[] = {&edges, &deg, &rid_of_gid, &gid_of_rid, &rkey, &off, &nbr, &pos, &hi, &eid,
+    DevBuf* bufs[] = {&edges, &deg, &rid_of_gid, &gid_of_rid, &rkey, &off, &nbr, &pos, &hi,
                       &wstart, &peel, &seglo, &seglen, &wpre, &items, &order, &bv, &acc, &kbuf, &be, &total, &orow, &otouch, &queue, &hub, &dflag, &split, &split_off, &split_cnt, &pieces, &srow, &slist,
                       &tmp_a, &tmp_b, &tmp_c, &tmp_d, &tmp_e, &tmp_f, &tmp_scan};
     for (DevBuf* b : bufs) f(*b);

@@ -1,5 +1,6 @@
 // bf_prims.cu -- hand-written device primitives for the CSR builder (layer B0):
-// exclusive prefix scan (reduce-then-scan, recursive over tile sums) and a
+// exclusive prefix scan (one tile: one CTA; else a single pass with decoupled
+// look-back) and a
 // stable LSD radix sort (<= 8-bit digits: tile histogram -> digit-major scan ->
 // stable scatter through shared memory).  Paper: "prefix sum" P:256-262 and
 // "parallel integer sort" P:668-677 (§2, §4.1).
@@ -21,22 +22,6 @@ size_t scan_levels_elems(size_t n) {
     n = t;
   }
   return tot + 2;
-}
-
-template <class TI, class TO>
-__global__ void __launch_bounds__(SCAN_THREADS) k_tile_reduce(const TI* __restrict__ in, size_t n,
-                                                              TO* __restrict__ tile_sums) {
-  __shared__ TO wt[32];
-  size_t base = (size_t)blockIdx.x * SCAN_TILE;
-  TO s = 0;
-#pragma unroll
-  for (int i = 0; i < SCAN_ITEMS; i++) {
-    size_t idx = base + (size_t)i * SCAN_THREADS + threadIdx.x;
-    if (idx < n) s += (TO)in[idx];
-  }
-  TO tot;
-  block_exclusive_scan<TO>(s, wt, &tot);
-  if (threadIdx.x == 0) tile_sums[blockIdx.x] = tot;
 }
 
 template <class TI, class TO>
@@ -80,6 +65,92 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_tile_scan(const TI* __restrict
 template <class TO>
 __global__ void k_set_scalar(TO* p, TO v) { *p = v; }
 
+// Single-pass exclusive scan with decoupled look-back: each CTA takes the next
+// tile (an atomic ticket, so every earlier tile is already running), publishes
+// its aggregate, sums its predecessors' published values backwards until an
+// inclusive prefix, publishes its own inclusive prefix and scans its tile.
+// Status words: flag (bits 62-63: 1 aggregate, 2 inclusive prefix) | value
+// (< 2^62); the status array and the ticket are zeroed before the launch.
+constexpr unsigned long long LB_AGG = 1ull << 62, LB_INC = 2ull << 62, LB_VAL = (1ull << 62) - 1;
+
+template <class TI, class TO>
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_lookback(const TI* __restrict__ in, TO* __restrict__ out,
+                                                                size_t n, TO* __restrict__ total,
+                                                                unsigned long long* __restrict__ status,
+                                                                uint32_t* __restrict__ ticket) {
+  __shared__ TO buf[SCAN_TILE];
+  __shared__ TO wt[32];
+  __shared__ uint32_t s_tile;
+  __shared__ TO s_prefix;
+  if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const size_t base = (size_t)tile * SCAN_TILE;
+#pragma unroll
+  for (int i = 0; i < SCAN_ITEMS; i++) {
+    const size_t idx = base + (size_t)i * SCAN_THREADS + threadIdx.x;
+    buf[i * SCAN_THREADS + threadIdx.x] = idx < n ? (TO)in[idx] : (TO)0;
+  }
+  __syncthreads();
+  TO v[SCAN_ITEMS];
+  TO sum = 0;
+#pragma unroll
+  for (int i = 0; i < SCAN_ITEMS; i++) {
+    v[i] = buf[threadIdx.x * SCAN_ITEMS + i];
+    sum += v[i];
+  }
+  TO agg;
+  TO ex = block_exclusive_scan<TO>(sum, wt, &agg);
+  if (threadIdx.x < 32) {  // warp 0: publish, look back, publish the inclusive prefix
+    const uint32_t lane = threadIdx.x;
+    if (tile == 0) {
+      if (lane == 0) {
+        atomicExch(status, LB_INC | (unsigned long long)agg);
+        s_prefix = 0;
+      }
+    } else {
+      if (lane == 0) atomicExch(status + tile, LB_AGG | (unsigned long long)agg);
+      unsigned long long prefix = 0;
+      int64_t j = (int64_t)tile - 1 - lane;  // this lane's predecessor in the window
+      for (;;) {
+        unsigned long long w = 0;
+        if (j >= 0) {
+          do { w = atomicAdd(status + j, 0ull); } while ((w >> 62) == 0);
+        } else {
+          w = LB_INC;  // before tile 0: an inclusive prefix of 0
+        }
+        const uint32_t inc = __ballot_sync(0xffffffffu, (w >> 62) == 2);
+        // lanes up to and including the nearest inclusive predecessor contribute
+        const uint32_t upto = inc ? (uint32_t)(__ffs(inc) - 1) : 31u;
+        unsigned long long mine = lane <= upto ? (w & LB_VAL) : 0ull;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+        prefix += mine;
+        if (inc) break;
+        j -= 32;
+      }
+      if (lane == 0) {
+        atomicExch(status + tile, LB_INC | ((prefix + (unsigned long long)agg) & LB_VAL));
+        s_prefix = (TO)prefix;
+      }
+    }
+  }
+  __syncthreads();
+  ex += s_prefix;
+#pragma unroll
+  for (int i = 0; i < SCAN_ITEMS; i++) {
+    buf[threadIdx.x * SCAN_ITEMS + i] = ex;
+    ex += v[i];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < SCAN_ITEMS; i++) {
+    const size_t idx = base + (size_t)i * SCAN_THREADS + threadIdx.x;
+    if (idx < n) out[idx] = buf[i * SCAN_THREADS + threadIdx.x];
+  }
+  if (total && (size_t)(tile + 1) * SCAN_TILE >= n && threadIdx.x == 0) *total = s_prefix + agg;
+}
+
 template <class TI, class TO>
 void scan_impl(const TI* in, TO* out, size_t n, TO* total, TO* temp, cudaStream_t s, uint64_t* launches) {
   if (n == 0) {
@@ -93,13 +164,11 @@ void scan_impl(const TI* in, TO* out, size_t n, TO* total, TO* temp, cudaStream_
     CUDA_TRY(cudaGetLastError());
     return;
   }
-  TO* sums = temp;
-  TO* rest = temp + tiles + 2;
-  k_tile_reduce<TI, TO><<<(unsigned)tiles, SCAN_THREADS, 0, s>>>(in, n, sums);
-  (*launches)++;
-  CUDA_TRY(cudaGetLastError());
-  scan_impl<TO, TO>(sums, sums, tiles, (TO*)nullptr, rest, s, launches);
-  k_tile_scan<TI, TO><<<(unsigned)tiles, SCAN_THREADS, 0, s>>>(in, out, n, sums, total);
+  // single pass with decoupled look-back: status words + ticket, zeroed here
+  unsigned long long* status = (unsigned long long*)temp;
+  uint32_t* ticket = (uint32_t*)(status + tiles);
+  CUDA_TRY(cudaMemsetAsync(status, 0, tiles * 8 + 8, s));
+  k_scan_lookback<TI, TO><<<(unsigned)tiles, SCAN_THREADS, 0, s>>>(in, out, n, total, status, ticket);
   (*launches)++;
   CUDA_TRY(cudaGetLastError());
 }
@@ -149,28 +218,24 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_upsweep(const K* __restrict__
   }
 }
 
-// the last pass of the slot sort may write the decoded CSR instead of keys and
-// values.  A slot's record is either (key, value) with value = slot id, or one
-// u64 key | edge id (Be low bits; the slot id is 2e + side) when both fit.
+// The last pass of each half of the slot sort writes the decoded CSR instead
+// of keys.  U half: records (src - src_base) << B | (nbr_last - nbr); besides
+// nbr and src it writes, for the slot at position p, the V half's input record
+// at m-1-p: (nbr - tbase) << Be | p -- the twin slot keyed by its source v with
+// the U position as payload.  Reversed, the U half runs in descending u, so a
+// stable sort of these records on the v field alone orders the V half.  V half:
+// records v_local << Be | p; the twin's source u = usrc[p] (the U half's src),
+// and knowing both twins' positions p and q it writes pos[q] = p - off[u]
+// (index of v in N(u)) and pos[p] = q - off[v] (index of u in N(v)).
 struct RadixDecode {
-  uint32_t* nbr;    // nbr[p] = nbr_last - (key & low B bits)
-  uint32_t* src;    // src[p] = src_base + (key >> B)
-  uint32_t* eid;    // U half: eid[p] = input edge id of the slot at p
-  uint32_t* pos;    // V half: twin positions (see below); global CSR positions
-  const uint32_t* off;
-  uint64_t nbr_last, src_base, pos_base;
+  uint32_t* nbr;         // range-local
+  uint32_t* src;         // range-local
+  uint32_t* pos;         // V half: global
+  const uint32_t* off;   // V half
+  const uint32_t* usrc;  // V half: the U half's src (global positions < m)
+  uint64_t* tkeys;       // U half: the V half's input records
+  uint64_t nbr_last, src_base, pos_base, tm, tbase;
   int B, Be, side;
-  // U half: also write the V half's input, transposed and reversed -- record
-  // m-1-p holds the twin slot (nbr -> src) keyed ((nbr - tbase) << tB | (tbase
-  // - 1 - src)) with the U position p as payload ([<< Be | p] or value p), so a
-  // stable sort on its high field alone orders the V half (the low field is
-  // already descending src).  The V half's last pass then knows both twins'
-  // positions p and q: pos[q] = p - off[u] (index of v in N(u)) and pos[p] =
-  // q - off[v] (index of u in N(v)) -- Alg. 1's twin indices with no search.
-  uint64_t* tkeys;
-  uint32_t* tvals;
-  uint64_t tm, tbase;
-  int tB;
 };
 
 #ifndef BF_RS_MINB
@@ -244,32 +309,26 @@ __global__ void __launch_bounds__(RS_THREADS, BF_RS_MINB) k_rs_downsweep(const K
   }
   __syncthreads();
   uint32_t cnt = (uint32_t)min((size_t)RS_TILE, n - tbase);
-  if (dec.nbr) {  // final pass of the slot sort: decode in place of the key/value write
-    const uint64_t lmask = (dec.B >= 64) ? ~0ull : ((1ull << dec.B) - 1);
+  if (!VALS && dec.nbr) {  // final pass of the slot sort: decode in place of the key write
+    const uint64_t lmask = (1ull << dec.B) - 1;
     const uint64_t emask = (1ull << dec.Be) - 1;
     for (uint32_t i = tid; i < cnt; i += RS_THREADS) {
       const uint64_t kr = (uint64_t)skeys[i];
       const uint32_t d = (uint32_t)(kr >> shift) & mask;
       const size_t gp = (uint32_t)(goff[d] + i);
-      const uint64_t k = kr >> dec.Be;
-      const uint32_t payload = VALS ? svals[i] : (uint32_t)(kr & emask);  // U: edge id; V: U position
-      const uint32_t nb = (uint32_t)(dec.nbr_last - (k & lmask)), sr = (uint32_t)(dec.src_base + (k >> dec.B));
-      dec.nbr[gp] = nb;
-      dec.src[gp] = sr;
-      if (dec.tkeys) {  // U half
-        dec.eid[gp] = payload;
-        const uint64_t tk = ((uint64_t)(nb - dec.tbase) << dec.tB) | (dec.tbase - 1 - sr);
-        const size_t tp = dec.tm - 1 - gp;
-        if (VALS) {
-          dec.tkeys[tp] = tk;
-          dec.tvals[tp] = (uint32_t)gp;
-        } else {
-          dec.tkeys[tp] = (tk << dec.Be) | gp;
-        }
-      } else {  // V half: q = pos_base + gp, twin at U position payload
+      if (dec.side == 0) {  // U half
+        const uint32_t nb = (uint32_t)(dec.nbr_last - (kr & lmask)), sr = (uint32_t)(dec.src_base + (kr >> dec.B));
+        dec.nbr[gp] = nb;
+        dec.src[gp] = sr;
+        dec.tkeys[dec.tm - 1 - gp] = ((uint64_t)(nb - dec.tbase) << dec.Be) | gp;
+      } else {  // V half: q = pos_base + gp, twin at U position p
+        const uint32_t p = (uint32_t)(kr & emask);
+        const uint32_t v = (uint32_t)(dec.src_base + (kr >> dec.Be)), u = __ldg(dec.usrc + p);
         const uint32_t q = (uint32_t)(dec.pos_base + gp);
-        dec.pos[q] = payload - __ldg(dec.off + nb);
-        dec.pos[payload] = q - __ldg(dec.off + sr);
+        dec.nbr[gp] = u;
+        dec.src[gp] = v;
+        dec.pos[q] = p - __ldg(dec.off + u);
+        dec.pos[p] = q - __ldg(dec.off + v);
       }
     }
     return;
@@ -297,7 +356,7 @@ int radix_impl(K* k0, uint32_t* v0, K* k1, uint32_t* v1, size_t n, int begin_bit
   K* ki = k0; K* ko = k1;
   uint32_t* vi = v0; uint32_t* vo = v1;
   int which = 0;
-  const RadixDecode none = {nullptr, nullptr, nullptr, nullptr, nullptr, 0, 0, 0, 0, 0, 0, nullptr, nullptr, 0, 0, 0};
+  const RadixDecode none = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0, 0, 0, 0, 0, 0, 0, 0};
   for (int p = 0, sh = begin_bit; p < passes; p++, sh += bits) {
     RadixDecode d = (dec && p == passes - 1) ? *dec : none;
     k_rs_upsweep<K><<<ntiles, RS_THREADS, 0, s>>>(ki, n, sh, bits, counts, ntiles);
@@ -343,18 +402,14 @@ int radix_sort_u64(uint64_t* k0, uint32_t* v0, uint64_t* k1, uint32_t* v1, size_
                    void* temp, cudaStream_t s, uint64_t* launches) {
   return radix_impl<uint64_t>(k0, v0, k1, v1, n, begin_bit, end_bit, temp, s, launches);
 }
-void radix_sort_slots(uint64_t* k0, uint32_t* v0, uint64_t* k1, uint32_t* v1, size_t n, int key_bits, int skip_bits,
-                      int B, int Be, uint64_t nbr_last, uint64_t src_base, uint64_t pos_base, uint32_t* nbr,
-                      uint32_t* src, uint32_t* eid, uint32_t* pos, const uint32_t* off, const SlotTranspose* tr,
-                      void* temp, cudaStream_t s, uint64_t* launches) {
-  RadixDecode dec = {nbr, src, eid, pos, off, nbr_last, src_base, pos_base, B, Be, tr ? 0 : 1, nullptr, nullptr, 0, 0, 0};
-  if (tr) {
-    dec.tkeys = tr->keys;
-    dec.tvals = tr->vals;
-    dec.tm = n;
-    dec.tbase = tr->base;
-    dec.tB = tr->B;
-  }
-  if (Be) radix_impl<uint64_t>(k0, nullptr, k1, nullptr, n, Be + skip_bits, Be + key_bits, temp, s, launches, &dec);
-  else radix_impl<uint64_t>(k0, v0, k1, v1, n, skip_bits, key_bits, temp, s, launches, &dec);
+void radix_sort_slots_u(uint64_t* k0, uint64_t* k1, size_t m, int Bu, int Bv, int Be, uint64_t n, uint32_t* nbr,
+                        uint32_t* src, uint64_t* vrec, uint64_t nU, void* temp, cudaStream_t s, uint64_t* launches) {
+  RadixDecode dec = {nbr, src, nullptr, nullptr, nullptr, vrec, n - 1, 0, 0, m, nU, Bv, Be, 0};
+  radix_impl<uint64_t>(k0, nullptr, k1, nullptr, m, 0, Bu + Bv, temp, s, launches, &dec);
+}
+void radix_sort_slots_v(uint64_t* k0, uint64_t* k1, size_t m, int Bv, int Be, uint64_t nU, uint32_t* nbr,
+                        uint32_t* src, uint32_t* pos, const uint32_t* off, const uint32_t* usrc, void* temp,
+                        cudaStream_t s, uint64_t* launches) {
+  RadixDecode dec = {nbr, src, pos, off, usrc, nullptr, 0, nU, m, 0, 0, 0, Be, 1};
+  radix_impl<uint64_t>(k0, nullptr, k1, nullptr, m, Be, Be + Bv, temp, s, launches, &dec);
 }

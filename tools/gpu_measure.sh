@@ -17,4 +17,11 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 bash tools/ncu_kernel.sh ${tag}_ncu_c4 "k_(big|small|split_walk|split_fin)" 5 5 --config 4
 bash tools/ncu_kernel.sh ${tag}_ncu_c3 "k_(big|small)" 3 3 --config 3 --mode edge
 bash tools/ncu_kernel.sh ${tag}_ncu_c5 "k_(big|small)" 3 3 --config 5
+# keep gpurun_out small (it must come back under 64 MiB): raw-page CSVs of every capture, the
+# c2 report itself only
+for r in gpurun_out/${tag}_ncu_c*.ncu-rep; do
+  ncu -i $r --page raw --csv > ${r%.ncu-rep}_raw.csv 2>/dev/null
+  case $r in *_ncu_c2.ncu-rep) ;; *) rm -f $r ;; esac
+done
+du -sh gpurun_out
 BF_LIB=libbf_debug.so timeout 2400 python tools/dbg_triage.py > gpurun_out/${tag}_debug_triage.log 2>&1; echo triage_rc=$?; tail -1 gpurun_out/${tag}_debug_triage.log
