@@ -57,12 +57,18 @@ def main():
         res = ncu_summary.load(a.ncu)
         dram = t_ms = inst = 0.0
         issue, l2 = [], []
+        import math
+        missing = []
         for r in res:
-            b = sum(qty(r[k], UNITS) for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
-            r["dram_bytes"] = b
-            dram += b
             t = qty(r["gpu__time_duration.sum"], TUNITS)
             t_ms += t
+            b = sum(qty(r[k], UNITS) for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+            if math.isnan(b):  # ncu returned no value for this launch's counters
+                missing.append(r["kernel"][:60])
+                r["dram_bytes"] = None
+                continue
+            r["dram_bytes"] = b
+            dram += b
             inst += float(r["smsp__inst_executed.sum"].split()[0])
             issue.append((t, float(r["smsp__issue_active.avg.pct_of_peak_sustained_active"].split()[0])))
             l2.append((b, float(r["lts__t_sector_hit_rate.pct"].split()[0])))
@@ -73,11 +79,12 @@ def main():
                           "-k regex:<wedge kernels> (one count call) python bench.py --steps 1 --warmup 1",
                "dram_bytes_per_launch": dram, "kernel_ms": t_ms,
                "l2_hit_pct": wsum(l2), "issue_active_pct": wsum(issue),
-               "warp_inst_per_wedge": inst / W if W else None,
+               "warp_inst_per_wedge": (inst / W if W else None) if not missing else None,
                "limiter": "L1/shared-memory wavefronts, shared-atomic latency and issue (see per-kernel stalls); "
                           "DRAM is not the binding unit",
                "note": "one bf_count call = one launch each of the kernels listed; bytes, time and instructions "
                        "summed over them (ncu serialises and flushes caches: shares matter, not absolutes)",
+               "counters_missing_for": missing,
                "kernels": res}
         json.dump(out, open(os.path.join(p, f"{base}_ncu_full.json"), "w"), indent=1)
         print(f"{base}: dram {dram / 1e9:.3f} GB, kernels {t_ms:.3f} ms, L2 hit {wsum(l2):.1f}%, "
