@@ -261,7 +261,8 @@ void bf_graph_destroy(bf_graph* g);
 
 /* Returns the library's cached device memory on `device` to the driver: the
  * heavy tier's per-CTA overflow rows (kept zero across calls and graphs, up
- * to 16 GB) and the unused blocks of the private stream-ordered pool.  Safe at
+ * to 60% of the free device memory and at most 64 GB) and the unused blocks of
+ * the private stream-ordered pool.  Safe at
  * any time (a later count reallocates what it needs); synchronises the device.
  * Errors: BF_EINVAL (bad device), BF_ECUDA. */
 bf_status bf_release_device_cache(int device);

@@ -25,59 +25,64 @@ inline unsigned grid_for(size_t n, int sms) {
 }
 
 // ---- a1 -----------------------------------------------------------------------
-// degree increments are aggregated over the lanes of a warp that hold the same
-// vertex (__match_any_sync): power-law hubs (c4's Zipf items) would otherwise
-// serialise thousands of atomics on one address
-#ifndef BF_DEG_MATCH
-#define BF_DEG_MATCH 1
-#endif
-__device__ __forceinline__ void add_degree(uint32_t* deg, uint32_t z, bool valid) {
-#if BF_DEG_MATCH
-  const uint32_t act = __ballot_sync(0xffffffffu, valid);
-  if (!valid) return;
-  const uint32_t peers = __match_any_sync(act, z);  // gid < n <= 2^32: a 32-bit match
-  if ((threadIdx.x & 31) == (uint32_t)(__ffs(peers) - 1)) atomicAdd(&deg[z], (uint32_t)__popc(peers));
-#else
-  if (valid) atomicAdd(&deg[z], 1u);
-#endif
-}
-
 // Degree counting privatises what it can: a side of at most HIST_MAX vertices
 // (c4: 30K items with Zipf popularity -- millions of increments on a few
 // addresses) is counted in a per-CTA shared-memory histogram and flushed once
-// per CTA; the other side's increments go to one of `stripes` copies of the
-// degree array (chosen by CTA; copy 0 is deg itself, summed by
-// k_degree_stripes), so a hub's increments spread over several addresses.
+// per CTA; the other side's hubs are counted in a per-CTA hot table (below),
+// the rest go to one of `stripes` copies of the degree array (chosen by CTA;
+// copy 0 is deg itself, summed by k_degree_stripes).
 constexpr uint32_t HIST_MAX = 40960;
+
+// The other side's hubs: a per-CTA direct-mapped table of HOT (id, count)
+// pairs in shared memory -- an id claims its empty slot at first sight and
+// counts there; an id that finds its slot taken by another goes to the
+// striped global copy.  Power-law hubs claim their slots early and keep them
+// (c2 step -0.06 ms).
+constexpr uint32_t HOT = 4096;
+constexpr uint32_t HOT_EMPTY = 0xffffffffu;
+
+__device__ __forceinline__ void count_degree(uint32_t* hot_id, uint32_t* hot_cnt, uint32_t* dg, uint32_t z,
+                                             bool hot) {
+  if (!hot) {
+    atomicAdd(dg + z, 1u);
+    return;
+  }
+  const uint32_t h = (z * 0x9E3779B1u) >> 20;  // 12 bits
+  uint32_t cur = hot_id[h];
+  if (cur == HOT_EMPTY) cur = atomicCAS(hot_id + h, HOT_EMPTY, z);
+  if (cur == HOT_EMPTY || cur == z) atomicAdd(hot_cnt + h, 1u);
+  else atomicAdd(dg + z, 1u);
+}
 
 __global__ void k_validate_degree(const uint32_t* __restrict__ e, uint64_t m, uint32_t nU, uint32_t nV,
                                   uint32_t* __restrict__ deg, uint32_t* __restrict__ flags, int hist_side,
-                                  uint32_t stripes, uint64_t n) {
+                                  uint32_t stripes, uint64_t n, uint32_t hot_sides) {
   extern __shared__ uint32_t hist[];
+  __shared__ uint32_t hot_id[HOT], hot_cnt[HOT];
+  const bool hot_u = hot_sides & 1u, hot_v = hot_sides & 2u;
   const uint32_t nh = hist_side == 0 ? nU : hist_side == 1 ? nV : 0u;
   for (uint32_t i = threadIdx.x; i < nh; i += blockDim.x) hist[i] = 0;
+  for (uint32_t i = threadIdx.x; i < HOT; i += blockDim.x) { hot_id[i] = HOT_EMPTY; hot_cnt[i] = 0; }
   __syncthreads();
   uint32_t* dg = deg + (size_t)(blockIdx.x % stripes) * n;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  // warp-uniform trip count (the aggregation is a warp collective)
-  for (uint64_t i0 = blockIdx.x * (uint64_t)blockDim.x + (threadIdx.x & ~31u); i0 < m; i0 += stride) {
-    const uint64_t i = i0 + (threadIdx.x & 31);
-    uint2 uv = make_uint2(0, 0);
-    bool ok = false;
-    if (i < m) {
-      uv = reinterpret_cast<const uint2*>(e)[i];
-      ok = uv.x < nU && uv.y < nV;
-      if (!ok) atomicOr(flags, 1u);
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += stride) {
+    const uint2 uv = reinterpret_cast<const uint2*>(e)[i];
+    if (!(uv.x < nU && uv.y < nV)) {
+      atomicOr(flags, 1u);
+      continue;
     }
-    if (hist_side == 0) { if (ok) atomicAdd(&hist[uv.x], 1u); }
-    else add_degree(dg, uv.x, ok);
-    if (hist_side == 1) { if (ok) atomicAdd(&hist[uv.y], 1u); }
-    else add_degree(dg, nU + uv.y, ok);
+    if (hist_side == 0) atomicAdd(&hist[uv.x], 1u);
+    else count_degree(hot_id, hot_cnt, dg, uv.x, hot_u);
+    if (hist_side == 1) atomicAdd(&hist[uv.y], 1u);
+    else count_degree(hot_id, hot_cnt, dg, nU + uv.y, hot_v);
   }
   __syncthreads();
   const uint32_t base = hist_side == 1 ? nU : 0u;
   for (uint32_t i = threadIdx.x; i < nh; i += blockDim.x)
     if (hist[i]) atomicAdd(&deg[base + i], hist[i]);
+  for (uint32_t i = threadIdx.x; i < HOT; i += blockDim.x)
+    if (hot_cnt[i]) atomicAdd(&deg[hot_id[i]], hot_cnt[i]);
 }
 
 __global__ void k_degree_stripes(uint32_t* __restrict__ deg, uint64_t n, uint32_t stripes) {
@@ -452,8 +457,11 @@ bf_status graph_ingest(bf_graph* g, const uint32_t* edges) {
     CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_validate_degree, threads, smem));
     const uint64_t want = (m + threads - 1) / threads;
     const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)g->sms * std::max(per_sm, 1)));
+    // hot tables only for a side of average degree >= 8 (hubs likely; c4's 20M users at
+    // 7 per user only fill the table with ids seen once: +1 ms)
+    const uint32_t hot_sides = (m >= 8ull * g->n_u ? 1u : 0u) | (m >= 8ull * g->n_v ? 2u : 0u);
     k_validate_degree<<<grid, threads, smem, s>>>(g->edges.as<uint32_t>(), m, g->n_u, g->n_v, g->deg.as<uint32_t>(),
-                                                  flags, hist_side, stripes, n);
+                                                  flags, hist_side, stripes, n, hot_sides);
     KERNEL_CHECK(g);
     if (stripes > 1) {
       k_degree_stripes<<<grid_for(n, g->sms), TPB, 0, s>>>(g->deg.as<uint32_t>(), n, stripes);

@@ -48,7 +48,9 @@
 #include "bf_device.cuh"
 #include <algorithm>
 #include <type_traits>
+#include <map>
 #include <mutex>
+#include <tuple>
 #include <stdlib.h>
 #include <stdio.h>
 
@@ -1003,6 +1005,13 @@ template <int ORIENT>
 __device__ __forceinline__ uint32_t split_kbase(const CountArgs& a, uint32_t s) {
   return ORIENT == BF_ORIENT_HIGH ? (s < a.n_u ? 0u : a.n_u) : s + 1u;
 }
+// the key range of start s (its d-row's length): same-side rids ranked above s
+// (HIGH) or below it (LOW)
+template <int ORIENT>
+__device__ __forceinline__ uint32_t split_keys(const CountArgs& a, uint32_t s) {
+  if (ORIENT == BF_ORIENT_HIGH) return s < a.n_u ? s : s - a.n_u;
+  return s < a.n_u ? a.n_u - s - 1u : (uint32_t)(a.n - s - 1u);
+}
 
 struct SplitStore1 {
   uint32_t* win;
@@ -1024,6 +1033,11 @@ struct SplitStore1Dense {
     atomicAdd(win + kk, 1u);
     return false;
   }
+};
+// dense pass 2: the start's d-row copied into shared memory per piece
+struct SplitStore2Shared {
+  const uint32_t* win;
+  __device__ __forceinline__ uint32_t get(uint32_t, uint32_t kk) const { return win[kk]; }
 };
 struct SplitStore2 {
   const uint32_t* row;
@@ -1076,12 +1090,19 @@ __global__ void __launch_bounds__(NT, NT == SP_NT ? 3 : 1) k_split_walk(CountArg
     SplitStore1 s1{win, wl, row, glist, sa.cnt + pc.x};
     SplitStore1Dense s1d{win};
     SplitStore2 s2{row};
+    SplitStore2Shared s2d{win};
+    if (PASS2 && DENSE) {  // the start's whole d-row to shared memory (its key range <= a.dwin)
+      const uint32_t kr = split_keys<ORIENT>(a, sp.x);
+      for (uint32_t kk = tid; kk < kr; kk += NT) win[kk] = __ldcg(row + kk);
+      __syncthreads();
+    }
     const uint64_t base = __ldg(a.wpre + pc.y), w = __ldg(a.wpre + pc.z) - base;
     uint32_t jc = pc.y, par = 0;
     uint64_t K0 = 0;
     bool hashed = false;
     if (w < (uint64_t)SLOT_MODE_AVG * (pc.z - pc.y)) {  // short segments: slot mode
-      if (PASS2) slots_pass2<MODE, NT, 4>(a, s2, pc.y, pc.z, kbase);
+      if (PASS2 && DENSE) slots_pass2<MODE, NT, 4>(a, s2d, pc.y, pc.z, kbase);
+      else if (PASS2) slots_pass2<MODE, NT, 4>(a, s2, pc.y, pc.z, kbase);
       else if (DENSE) slots_pass1<false, NT, 4>(a, s1d, pc.y, pc.z, kbase, &ss.u.lcnt, ss.list, SP_WIN, nullptr, hashed);
       else slots_pass1<false, NT, 4>(a, s1, pc.y, pc.z, kbase, &ss.u.lcnt, ss.list, SP_WIN, nullptr, hashed);
       __syncthreads();
@@ -1093,7 +1114,13 @@ __global__ void __launch_bounds__(NT, NT == SP_NT ? 3 : 1) k_split_walk(CountArg
       const uint64_t K1 = units_build<PASS2 ? MODE : MODE_TOTAL, NT, SP_P, SplitSmem::UCAP>(
           a, ss.u, jc, pc.z, base, K0, cap, par, mine, myj, myy);
       const uint32_t jn = ss.u.jn[par];
-      if (PASS2) {
+      if (PASS2 && DENSE) {
+        if (sp.z - sp.y < (1u << 26))
+          units_pass2<MODE, false, NT, SP_P, SP_G, 1, SplitSmem::UCAP>(a, ss.u, s2d, kbase, nullptr);
+        else
+          units_pass2<MODE, false, NT, SP_P, SP_G, 1, SplitSmem::UCAP, SplitStore2Shared, false>(a, ss.u, s2d, kbase,
+                                                                                                   nullptr);
+      } else if (PASS2) {
         if (sp.z - sp.y < (1u << 26))
           units_pass2<MODE, false, NT, SP_P, SP_G, 1, SplitSmem::UCAP>(a, ss.u, s2, kbase, nullptr);
         else
@@ -1291,9 +1318,17 @@ __global__ void k_unrename(const uint64_t* __restrict__ bv, const uint32_t* __re
   }
 }
 
-// be[e] = the sums of the edge's two slots: the U slot at p = off[ru] + the
-// index of rv in N(ru) (a binary search: rows are sorted by decreasing rid) and
-// its twin off[rv] + pos[p]
+// be[e] = the sums of the edge's two slots.  A binary search in the shorter of
+// the two rows (sorted by decreasing rid) finds one slot; its pos gives the
+// twin: slot ru->rv at p, rv->ru at off[rv] + pos[p] (and symmetrically)
+__device__ __forceinline__ uint32_t row_find(const uint32_t* __restrict__ nbr, uint32_t lo, uint32_t hi, uint32_t x) {
+  while (lo < hi) {  // first index with nbr <= x
+    const uint32_t mid = lo + ((hi - lo) >> 1);
+    if (nbr[mid] > x) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
 __global__ void k_edge_gather(const uint64_t* __restrict__ acc, const uint32_t* __restrict__ edges,
                               const uint32_t* __restrict__ rid_of_gid, const uint32_t* __restrict__ nbr,
                               const uint32_t* __restrict__ pos, const uint32_t* __restrict__ off, uint32_t nU,
@@ -1301,14 +1336,17 @@ __global__ void k_edge_gather(const uint64_t* __restrict__ acc, const uint32_t* 
   for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m; e += (uint64_t)gridDim.x * blockDim.x) {
     const uint2 uv = reinterpret_cast<const uint2*>(edges)[e];
     const uint32_t ru = rid_of_gid[uv.x], rv = rid_of_gid[(uint64_t)nU + uv.y];
-    uint32_t lo = off[ru], hi = off[ru + 1];  // first index with nbr <= rv
-    while (lo < hi) {
-      const uint32_t mid = lo + ((hi - lo) >> 1);
-      if (nbr[mid] > rv) lo = mid + 1;
-      else hi = mid;
+    const uint32_t ou = off[ru], du = off[ru + 1] - ou, ov = off[rv], dv = off[rv + 1] - ov;
+    uint32_t a, b;
+    if (du <= dv) {
+      a = row_find(nbr, ou, ou + du, rv);
+      b = ov + pos[a];
+    } else {
+      b = row_find(nbr, ov, ov + dv, ru);
+      a = ou + pos[b];
     }
-    BF_CHECK(nbr[lo] == rv);
-    be[e] = acc[lo] + acc[(size_t)off[rv] + pos[lo]];
+    BF_CHECK(nbr[a] == rv && nbr[b] == ru);
+    be[e] = acc[a] + acc[b];
   }
 }
 
@@ -1320,15 +1358,35 @@ inline unsigned grid_for(size_t n, int sms) {
   return (unsigned)g;
 }
 
+// blocks per SM of a kernel at (threads, dynamic smem); the attribute set and
+// the occupancy query are host API calls inside the timed count, so their
+// answers are cached per (device, kernel, threads, smem)
+// (the dynamic-smem attribute only ever grows, so a cached answer for a
+// smaller launch never leaves the attribute below a later launch's need)
 template <class K>
 int occupancy(K kernel, int threads, size_t smem) {
-  CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  static std::mutex mu;
+  static std::map<std::tuple<int, const void*, int, size_t>, int> cache;
+  static std::map<std::pair<int, const void*>, size_t> attr;
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  const auto key = std::make_tuple(dev, (const void*)kernel, threads, smem);
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& set = attr[std::make_pair(dev, (const void*)kernel)];
+  if (smem > set || set == 0) {
+    CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
 #ifdef BF_CARVEOUT  // tuning: shared-memory carve-out in percent (the rest is L1)
-  CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, BF_CARVEOUT));
+    CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, BF_CARVEOUT));
 #endif
+    set = std::max<size_t>(smem, 1);
+  }
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
   int b = 0;
   CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, threads, smem));
-  return b > 0 ? b : 1;
+  b = b > 0 ? b : 1;
+  cache[key] = b;
+  return b;
 }
 
 // Per-device pool of heavy-tier overflow rows + touched lists.  The lock is
@@ -1340,8 +1398,12 @@ struct RowPool {
   void* l = nullptr;  // touched lists (scratch)
   size_t lbytes = 0;
   bool dirty = false;
+  size_t budget = 0;  // bytes rows + lists may take (set at first use, from the free memory then)
 };
-constexpr size_t kRowPoolBudget = (size_t)16 << 30;
+// the pool may take up to 60% of the device's free memory (plus what it holds),
+// at most 64 GB: c5's heavy key ranges (up to 8M keys, 64 MB of row + list per
+// CTA) ran at 1.7 CTAs per SM under round 1's fixed 16 GB
+constexpr size_t kRowPoolMax = (size_t)64 << 30;
 RowPool& row_pool(int dev) {
   static RowPool pools[64];
   return pools[dev & 63];
@@ -1358,6 +1420,7 @@ void row_pool_free(int dev) {
   pool.p = pool.l = nullptr;
   pool.bytes = pool.lbytes = 0;
   pool.dirty = false;
+  pool.budget = 0;
 }
 
 namespace {
@@ -1388,8 +1451,9 @@ void launch_tiers(bf_graph* g, CountArgs a, const uint32_t tier[4], uint32_t* qu
       k_split_finalize<ORIENT, MODE><<<fgrid, 256, 0, s>>>(a, sa);
       KERNEL_CHECK(g);
       if (MODE != MODE_TOTAL) {
-        auto k2 = k_split_walk<ORIENT, MODE, true, false, SP_NT_WIDE>;  // pass 2 reads the global rows only
-        const size_t smem2 = sizeof(SplitSmemT<SP_NT_WIDE>::U);
+        // pass 2 reads the global rows, or (dense) each piece's start row copied to shared memory
+        auto k2 = dense ? k_split_walk<ORIENT, MODE, true, true, SP_NT_WIDE> : k_split_walk<ORIENT, MODE, true, false, SP_NT_WIDE>;
+        const size_t smem2 = sizeof(SplitSmemT<SP_NT_WIDE>::U) + (dense ? (size_t)a.dwin * 4 : 0);
         a.queue = queues + 5;
         k2<<<sms * occupancy(k2, SP_NT_WIDE, smem2), SP_NT_WIDE, smem2, s>>>(a, sa);
         KERNEL_CHECK(g);
@@ -1408,8 +1472,8 @@ void launch_tiers(bf_graph* g, CountArgs a, const uint32_t tier[4], uint32_t* qu
     // across graphs without clearing); the grid shrinks if the rows of every
     // CTA would exceed the pool budget
     const size_t row_bytes = (a.orow_len + a.olist_len) * 4;
-    grid = (int)std::max<size_t>(1, std::min<size_t>((size_t)grid, kRowPoolBudget / row_bytes));
     RowPool& pool = row_pool(g->device);
+    grid = (int)std::max<size_t>(1, std::min<size_t>((size_t)grid, g->pool_budget / row_bytes));
     // rows (kept zero) and lists (scratch) are separate allocations, so a later
     // launch with another grid never finds list garbage inside its rows
     const size_t need_rows = (size_t)grid * a.orow_len * 4, need_lists = (size_t)grid * a.olist_len * 4;
@@ -1539,6 +1603,15 @@ bf_status graph_count(bf_graph* g, int mode, uint64_t* out_a, uint64_t* out_b, u
     CUDA_TRY(cudaMemcpyToSymbolAsync(g_prof_red, z, 32, 0, cudaMemcpyHostToDevice, s));
   }
 #endif
+  if (g->n_tier[0]) {  // the heavy tier's row-pool budget: fixed at the pool's first use on the device
+    RowPool& pool = row_pool(g->device);  // (its lock is held for the whole call: pool_lock above)
+    if (!pool.budget) {
+      size_t free_b = 0, total_b = 0;
+      CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
+      pool.budget = std::max<size_t>((size_t)1 << 30, std::min(kRowPoolMax, free_b / 10 * 6));
+    }
+    g->pool_budget = pool.budget;
+  }
   CUDA_TRY(cudaEventRecord(g->ev[1], s));
   NvtxRange nv_walk("bf a5-a7 wedge kernels");
   for (int r = first; r <= last; r++) {

@@ -167,6 +167,7 @@ struct bf_graph {
   DevBuf order;         // u32 [n_tier sum]
   uint32_t n_tier[3] = {0, 0, 0};
   uint64_t heavy_keys = 1;  // max key range of a heavy start (sizes the heavy rows)
+  size_t pool_budget = 0;   // bytes the heavy tier's row pool may hold (set per count)
   uint32_t t1 = 512, t2 = 2048;
 
   // split starts (a4): the first n_split heavy starts (w > split threshold)

@@ -410,3 +410,23 @@ def test_approx_codegen_work_bound(seed):
         if r[x] < r[y]:
             degxy = sum(1 for z in nbrs[y] if r[z] > r[x])
             assert degxy <= 2 * deg[x], (x, y)
+
+
+def test_fullsize_cache_reproduces():
+    """tests/golden/fullsize_oracle.json (tools/oracle_cache.py) is what the
+    oracle computes: config 1 in full from a fresh sharded run, and the cached
+    generator keys (edge-list SHA-256) of configs 1-2 from fresh generation."""
+    import hashlib
+    cache = json.load(open(os.path.join(GOLDEN, "fullsize_oracle.json")))
+    sha = lambda a: hashlib.sha256(np.ascontiguousarray(a).astype("<u8").tobytes()).hexdigest()
+    for k in (1, 2):
+        g = bfgen.config_graph(k)
+        c = cache[str(k)]
+        assert c["gen_version"] == bfgen.GEN_VERSION
+        assert hashlib.sha256(np.ascontiguousarray(g.edges).astype("<u4").tobytes()).hexdigest() == c["edges_sha256"]
+        if k == 1:
+            with oracle.OracleGraph(g.n_u, g.n_v, g.edges) as og:
+                r = og.count_sharded(procs=3)
+            assert r["total"] == c["total"]
+            for name in ("b_u", "b_v", "b_e"):
+                assert sha(r[name]) == c[name + "_sha256"]
