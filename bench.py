@@ -486,11 +486,20 @@ def main():
     }
     if prof:
         dram_gbs = traffic / (prof["kernel_ms"] / 1e3) / 1e9 if traffic and prof.get("kernel_ms") else None
+        # instruction-issue ceiling: 4 warp schedulers per SM, one warp instruction each per cycle
+        clk_mhz = peaks.get("sm_max_mhz") or 1965.0
+        issue_peak = 148 * 4 * clk_mhz * 1e6
+        wipw = prof.get("warp_inst_per_wedge")
+        issue_rate = wipw * W / (t_kernel / 1e3) if wipw and t_kernel else None
         out["roofline"]["measured"] = {
             "source": prof["path"], "src_sha": prof.get("src_sha"), "matches_this_build": prof.get("matches"),
             "dram_bytes_per_launch": traffic, "dram_gbs": dram_gbs,
             "dram_frac": dram_gbs / peak if dram_gbs else None, "l2_hit_pct": prof.get("l2_hit_pct"),
-            "issue_active_pct": prof.get("issue_active_pct"), "warp_inst_per_wedge": prof.get("warp_inst_per_wedge"),
+            "issue_active_pct": prof.get("issue_active_pct"), "warp_inst_per_wedge": wipw,
+            "issue_rate_warp_inst_per_s": issue_rate, "issue_peak_warp_inst_per_s": issue_peak,
+            "issue_frac": issue_rate / issue_peak if issue_rate else None,
+            "issue_basis": "the capture's warp instructions per wedge x W / this run's wedge-kernel time, against "
+                           "148 SMs x 4 schedulers x max SM clock",
             "limiter": prof.get("limiter")}
         if not prof.get("matches"):
             out["roofline"]["traffic"] = None  # the profile is of other code: report it beside, not as this run's
