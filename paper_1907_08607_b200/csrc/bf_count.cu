@@ -182,7 +182,31 @@ __device__ __forceinline__ uint64_t* endpoint_slot(const CountArgs& a, uint32_t 
 // wraps.
 __device__ __forceinline__ uint32_t hslot(uint32_t key, uint32_t shift) { return (key * 0x9E3779B1u) >> shift; }
 
-struct SmallStore {
+// SCAN (BF_SMALL_SCAN bit 0: warp tier, bit 1: medium tier): increments are
+// fire-and-forget (red.shared), nothing records owners; finalize scans the
+// window's first nk counters and, when a key of the start was hashed, the hash
+// slots' counts.  (Measured on c2 for both tiers: wedge kernels 5.71 -> 6.67 ms
+// -- a warp-tier start has ~190 wedges against a 1024-counter window.)
+#ifndef BF_SMALL_SCAN
+#define BF_SMALL_SCAN 0
+#endif
+__device__ __forceinline__ void red_shared_u32(uint32_t* p, uint32_t v) {
+  asm volatile("red.shared.add.u32 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(p)), "r"(v) : "memory");
+}
+// endpoint pairs of four packed u8 counters (byte b of word wd is key offset
+// idx0 + b, or the key of hash slot idx0 + b): C(d,2) to the total and both endpoints
+template <int MODE>
+__device__ __forceinline__ void bytes_finalize(const CountArgs& a, uint32_t wd, uint32_t kbase, uint32_t idx0,
+                                               const uint32_t* hkeys, uint64_t& lsum, uint32_t& np);
+
+template <bool SCAN, bool OWN2 = false>
+struct SmallStoreT {
+  static constexpr bool kScan = SCAN;
+  // OWN2: the owner of a key is the wedge that takes its count from 1 to 2, so
+  // the list holds only the keys that contribute (d >= 2); a key seen once is
+  // reset in pass 2 by its only wedge (vertex / edge modes only)
+  static constexpr bool kOwn2 = OWN2;
+  uint32_t nk;    // SCAN: window counters the current start can touch (min(wl, its key range))
   uint32_t* win;  // u8 counters, four per word: bytes [0, WIN) the dense window (key kk: byte kk),
                   // bytes [WIN, WIN + HS) the hash slots' counts (slot h: byte WIN + h)
   uint32_t* hk;
@@ -211,8 +235,13 @@ struct SmallStore {
     }
     BF_CHECK(__isShared(win + (ci >> 2)));
     const uint32_t sh = (ci & 3u) << 3;
-    const uint32_t old = atomicAdd(win + (ci >> 2), 1u << sh);
-    return ((old >> sh) & 0xffu) == 0u;
+    if constexpr (SCAN) {
+      red_shared_u32(win + (ci >> 2), 1u << sh);
+      return false;
+    } else {
+      const uint32_t old = atomicAdd(win + (ci >> 2), 1u << sh);
+      return ((old >> sh) & 0xffu) == (OWN2 ? 1u : 0u);
+    }
   }
   __device__ __forceinline__ uint32_t at(uint32_t ci) const { return ((const uint8_t*)win)[ci]; }
   __device__ __forceinline__ void zero_at(uint32_t ci) const {
@@ -240,21 +269,104 @@ struct SmallStore {
     hk[h] = EMPTY;
     ((uint8_t*)win)[winb + h] = 0;
   }
+  // SCAN finalize: window bytes [0, nk), then (hany: some key of the start was
+  // hashed) the hash slots' counts
+  template <int MODE, int NT>
+  __device__ __forceinline__ void scan_finalize(const CountArgs& a, uint32_t kbase, bool hany, uint64_t& lsum,
+                                                uint64_t& pairs) const {
+    uint32_t np = 0;
+    const uint4* w4 = reinterpret_cast<const uint4*>(win);
+    const uint32_t nq = (nk + 15u) >> 4;
+    for (uint32_t q = threadIdx.x; q < nq; q += NT) {
+      const uint4 v = w4[q];
+      if ((v.x | v.y | v.z | v.w) == 0u) continue;
+      bytes_finalize<MODE>(a, v.x, kbase, 16u * q, nullptr, lsum, np);
+      bytes_finalize<MODE>(a, v.y, kbase, 16u * q + 4u, nullptr, lsum, np);
+      bytes_finalize<MODE>(a, v.z, kbase, 16u * q + 8u, nullptr, lsum, np);
+      bytes_finalize<MODE>(a, v.w, kbase, 16u * q + 12u, nullptr, lsum, np);
+    }
+    if (hany) {
+      const uint32_t hq = (hmask + 1u) >> 4;
+      for (uint32_t q = threadIdx.x; q < hq; q += NT) {
+        const uint4 v = w4[(winb >> 4) + q];
+        if ((v.x | v.y | v.z | v.w) == 0u) continue;
+        bytes_finalize<MODE>(a, v.x, 0u, 16u * q, hk, lsum, np);
+        bytes_finalize<MODE>(a, v.y, 0u, 16u * q + 4u, hk, lsum, np);
+        bytes_finalize<MODE>(a, v.z, 0u, 16u * q + 8u, hk, lsum, np);
+        bytes_finalize<MODE>(a, v.w, 0u, 16u * q + 12u, hk, lsum, np);
+      }
+    }
+    pairs += np;
+  }
+  template <int NT>
+  __device__ __forceinline__ void scan_reset(bool hany) const {
+    uint4* w4 = reinterpret_cast<uint4*>(win);
+    const uint32_t nq = (nk + 15u) >> 4;
+    for (uint32_t q = threadIdx.x; q < nq; q += NT) w4[q] = make_uint4(0u, 0u, 0u, 0u);
+    if (hany) {
+      const uint32_t hs = hmask + 1u;
+      for (uint32_t q = threadIdx.x; q < (hs >> 4); q += NT) w4[(winb >> 4) + q] = make_uint4(0u, 0u, 0u, 0u);
+      uint4* k4 = reinterpret_cast<uint4*>(hk);
+      for (uint32_t q = threadIdx.x; q < (hs >> 2); q += NT) k4[q] = make_uint4(EMPTY, EMPTY, EMPTY, EMPTY);
+    }
+  }
 };
+
+template <int MODE>
+__device__ __forceinline__ void bytes_finalize(const CountArgs& a, uint32_t wd, uint32_t kbase, uint32_t idx0,
+                                               const uint32_t* hkeys, uint64_t& lsum, uint32_t& np) {
+  while (wd) {
+    const uint32_t sh = (uint32_t)(__ffs(wd) - 1) & ~7u;
+    const uint32_t d = (wd >> sh) & 0xffu;
+    wd &= ~(0xffu << sh);
+    np++;
+    if (d > 1u) {
+      const uint32_t c2 = (d * (d - 1u)) >> 1;  // d <= 128
+      lsum += c2;
+      const uint32_t i = idx0 + (sh >> 3);
+      const uint32_t key = hkeys ? hkeys[i] : kbase + i;
+      if (MODE == MODE_VERTEX && !(a.exp & 1)) red_add_u64(endpoint_slot(a, key), c2);
+    }
+  }
+}
+#ifndef BF_SMALL_OWN2
+#define BF_SMALL_OWN2 1
+#endif
+template <int NT, int MODE>
+using SmallStore = SmallStoreT<((NT == 32 ? 1 : 2) & BF_SMALL_SCAN) != 0,
+                               BF_SMALL_OWN2 != 0 && BF_SMALL_SCAN == 0 && MODE != MODE_TOTAL>;
 
 // ------------------------------------------------ heavy counter store
 // u32 dense shared window over [0, wl) + the CTA's global row for the rest
 // (L2 atomics; plain reads bypass L1 so they see the atomics' results).
-struct HeavyStore {
+// SCAN: window increments are fire-and-forget (red.shared: no owner test, no
+// list push, nothing waits on the atomic's return); finalize and the reset
+// scan the window's first nk counters (the start's key range) instead of an
+// owner list -- only overflow-row keys keep owners.
+#ifndef BF_BIG_SCAN
+#define BF_BIG_SCAN 1
+#endif
+template <bool SCAN>
+struct HeavyStoreT {
+  static constexpr bool kScan = SCAN;
   uint32_t* win;
   uint32_t* orow;
   uint32_t wl;
+  uint32_t nk;  // SCAN: window counters the current start can touch (min(wl, its key range))
   uint64_t lenchk;
   // the window path is the common one (99.5% of heavy-tier keys on c2): a
   // real branch keeps the global row's address arithmetic off it
   __device__ __forceinline__ bool add(uint32_t, uint32_t kk, bool&) const {
     BF_CHECK(kk < wl || kk - wl < lenchk);
-    if (__builtin_expect(kk < wl, 1)) return atomicAdd(win + kk, 1u) == 0u;
+    BF_CHECK(!SCAN || kk >= wl || kk < nk);
+    if (__builtin_expect(kk < wl, 1)) {
+      if constexpr (SCAN) {
+        red_shared_u32(win + kk, 1u);
+        return false;
+      } else {
+        return atomicAdd(win + kk, 1u) == 0u;
+      }
+    }
     return atomicAdd(orow + (kk - wl), 1u) == 0u;
   }
   __device__ __forceinline__ uint32_t get(uint32_t, uint32_t kk) const {
@@ -265,7 +377,47 @@ struct HeavyStore {
     if (__builtin_expect(kk < wl, 1)) win[kk] = 0;
     else __stcg(orow + (kk - wl), 0u);
   }
+  // SCAN finalize: every non-zero counter of the window's first nk keys is one
+  // endpoint pair (the window part of the owner list): C(d,2) to the total and
+  // both endpoints, read four counters at a time
+  template <int MODE, int NT>
+  __device__ __forceinline__ void scan_finalize(const CountArgs& a, uint32_t kbase, bool, uint64_t& lsum,
+                                                uint64_t& pairs) const {
+    const uint32_t nq = (nk + 3u) >> 2;
+    const uint4* w4 = reinterpret_cast<const uint4*>(win);
+    uint32_t np = 0;
+    for (uint32_t q = threadIdx.x; q < nq; q += NT) {
+      const uint4 v = w4[q];
+      if ((v.x | v.y | v.z | v.w) == 0u) continue;
+      const uint32_t d[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int c = 0; c < 4; c++) {
+        np += d[c] != 0u;
+        if (d[c] > 1u) {
+          const uint64_t c2 = choose2(d[c]);
+          lsum += c2;
+          if (MODE == MODE_VERTEX && !(a.exp & 1)) red_add_u64(endpoint_slot(a, kbase + 4u * q + c), c2);
+        }
+      }
+    }
+    pairs += np;
+  }
+  template <int NT>
+  __device__ __forceinline__ void scan_reset(bool) const {
+    const uint32_t nq = (nk + 3u) >> 2;
+    uint4* w4 = reinterpret_cast<uint4*>(win);
+    for (uint32_t q = threadIdx.x; q < nq; q += NT) w4[q] = make_uint4(0u, 0u, 0u, 0u);
+  }
 };
+using HeavyStore = HeavyStoreT<BF_BIG_SCAN != 0>;
+
+// the key range of start s (same-side rids ranked above s (HIGH) or below it
+// (LOW)): every key offset kk of its wedges is below it
+template <int ORIENT>
+__device__ __forceinline__ uint32_t key_range(uint32_t s, uint32_t n_u, uint64_t n) {
+  if (ORIENT == BF_ORIENT_HIGH) return s < n_u ? s : s - n_u;
+  return s < n_u ? n_u - s - 1u : (uint32_t)(n - s - 1u);
+}
 
 // ================================================================ unit walk
 // A chunk of a start's wedge sequence is cut into "units": pieces of at most P
@@ -458,7 +610,8 @@ __device__ __forceinline__ void units_pass1(const CountArgs& a, Units<NT, UCAP>&
 // d-1 fits u32 and the group reduction shuffles 32-bit words
 template <int MODE, bool CACHE, int NT, int P, int G, int UR, uint32_t UCAP, class Store, bool NARROW = true>
 __device__ __forceinline__ void units_pass2(const CountArgs& a, Units<NT, UCAP>& u, const Store& cs,
-                                            uint32_t kbase, const uint16_t* cache) {
+                                            uint32_t kbase, const uint16_t* cache, uint64_t* np1 = nullptr) {
+  uint32_t ones = 0;  // OWN2: keys seen once (reset here by their only wedge)
   constexpr int IT = P / G;
   constexpr uint32_t NG = NT / G;
   const uint32_t tid = threadIdx.x, gl = tid & (G - 1);
@@ -489,8 +642,17 @@ __device__ __forceinline__ void units_pass2(const CountArgs& a, Units<NT, UCAP>&
       for (int it = 0; it < IT; it++) {
         if (key[r][it] != EMPTY) {
           uint32_t c;
-          if constexpr (CACHE) c = cs.at(key[r][it]) - 1u;
-          else c = cs.get(key[r][it], key[r][it] - kbase) - 1u;
+          if constexpr (CACHE) {
+            c = cs.at(key[r][it]) - 1u;
+            if constexpr (Store::kOwn2) {
+              if (c == 0u) {
+                cs.zero_at(key[r][it]);
+                ones++;
+              }
+            }
+          } else {
+            c = cs.get(key[r][it], key[r][it] - kbase) - 1u;
+          }
           s += c;
           if (MODE == MODE_EDGE && c) red_add_u64(a.acc + (lo[r] + gl + it * G), c);  // edge (y, key)
         }
@@ -500,6 +662,7 @@ __device__ __forceinline__ void units_pass2(const CountArgs& a, Units<NT, UCAP>&
       if (x < nunits && gl == 0 && s) seg_add(u.slo, u.shi, sl[r], (uint64_t)s);
     }
   }
+  if (np1) *np1 += ones;
 }
 
 template <int MODE>
@@ -575,7 +738,17 @@ __device__ __forceinline__ void start_passes(const CountArgs& a, Units<NT, UCAP>
   if (single) units_pass1<SPILL, CACHE, NT, P, G, UR, UCAP>(a, u, cs, st.kbase, list, lcap, olist, hashed, cache, listi);
   else units_pass1<SPILL, false, NT, P, G, UR, UCAP>(a, u, cs, st.kbase, list, lcap, olist, hashed, nullptr, nullptr);
   pf.mark(2);
-  cta_sync<NT>();
+  bool hany = false;  // SCAN: some key of the start went to the hash
+  if constexpr (Store::kScan) {
+    if (NT == 32) {
+      __syncwarp();
+      hany = __any_sync(FULL, hashed);
+    } else {
+      hany = __syncthreads_or(hashed) != 0;
+    }
+  } else {
+    cta_sync<NT>();
+  }
   pf.mark(3);
   if (!single) {
     if (tid == 0) u.jn[0] = FULL;
@@ -595,23 +768,26 @@ __device__ __forceinline__ void start_passes(const CountArgs& a, Units<NT, UCAP>
   pf.mark(1);
   const uint32_t cnt = u.lcnt;
   list_finalize<MODE, SPILL, NT>(a, cs, st.kbase, cnt, list, lcap, olist, lsum, CACHE ? listi : nullptr);
+  if constexpr (Store::kScan) cs.template scan_finalize<MODE, NT>(a, st.kbase, hany, lsum, pairs);
   if (tid == 0) pairs += cnt;
   pf.mark(4);
-  if (MODE == MODE_TOTAL && SPILL) {
+  if (MODE == MODE_TOTAL && (SPILL || Store::kScan)) {
     cta_sync<NT>();
-    for (uint32_t i = tid; i < cnt; i += NT) {
-      const uint32_t key = list_get<SPILL>(list, lcap, olist, i);
-      cs.zero(key, key - st.kbase);
-    }
+    if (SPILL)
+      for (uint32_t i = tid; i < cnt; i += NT) {
+        const uint32_t key = list_get<SPILL>(list, lcap, olist, i);
+        cs.zero(key, key - st.kbase);
+      }
+    if constexpr (Store::kScan) cs.template scan_reset<NT>(hany);
   }
   if (MODE != MODE_TOTAL) {
     cta_sync<NT>();  // d is final
     pf.mark(3);
     if (single) {
       if (st.j1 - st.j0 < (1u << 26))
-        units_pass2<MODE, CACHE, NT, P, G, UR, UCAP>(a, u, cs, st.kbase, cache);
+        units_pass2<MODE, CACHE, NT, P, G, UR, UCAP>(a, u, cs, st.kbase, cache, &pairs);
       else
-        units_pass2<MODE, CACHE, NT, P, G, UR, UCAP, Store, false>(a, u, cs, st.kbase, cache);
+        units_pass2<MODE, CACHE, NT, P, G, UR, UCAP, Store, false>(a, u, cs, st.kbase, cache, &pairs);
       pf.mark(5);
       cta_sync<NT>();
       pf.mark(3);
@@ -642,6 +818,7 @@ __device__ __forceinline__ void start_passes(const CountArgs& a, Units<NT, UCAP>
         cs.zero(key, key - st.kbase);
       }
     }
+    if constexpr (Store::kScan) cs.template scan_reset<NT>(hany);
   }
   pf.mark(6);
   cta_sync<NT>();
@@ -797,8 +974,8 @@ template <int NT, uint32_t WIN, uint32_t HS, uint32_t CAP, int P, int G, int UR>
 struct SmallSmem {
   static constexpr uint32_t UCAP = CAP / P + NT;
   Units<NT, UCAP> u;
-  uint32_t win[WIN / 4 + HS / 4];  // u8 counters: the dense window, then the hash slots' counts
-  uint32_t hk[HS];
+  alignas(16) uint32_t win[WIN / 4 + HS / 4];  // u8 counters: the dense window, then the hash slots' counts
+  alignas(16) uint32_t hk[HS];
   uint32_t list[SMALL_CACHE(NT) ? 1 : CAP];   // distinct keys <= w <= CAP (without the index cache)
   uint16_t listi[SMALL_CACHE(NT) ? CAP : 2];  // the owners' counter indices (with it)
   uint16_t cache[SMALL_CACHE(NT) ? CAP : 2];  // each wedge's counter index, in chunk order
@@ -829,8 +1006,9 @@ __global__ void __launch_bounds__(NT, NT == 32 ? 1 : BF_MED_MINB) k_small(CountA
   extern __shared__ __align__(16) char sm[];
   SM& ss = *(SM*)sm;
   const uint32_t tid = threadIdx.x, lane = tid & 31;
-  static_assert((HS & (HS - 1)) == 0 && (WIN & (WIN - 1)) == 0 && WIN >= 4, "store sizes");
-  SmallStore cs;
+  static_assert((HS & (HS - 1)) == 0 && (WIN & (WIN - 1)) == 0 && WIN >= 16 && HS >= 16, "store sizes (scans read 16 counters at a time)");
+  SmallStore<NT, MODE> cs;
+  static_assert(!decltype(cs)::kOwn2 || SMALL_CACHE(NT), "OWN2 resets once-seen keys through the counter-index cache");
   cs.win = ss.win;
   cs.hk = ss.hk;
   cs.hv = ss.win + WIN / 4;
@@ -867,6 +1045,7 @@ __global__ void __launch_bounds__(NT, NT == 32 ? 1 : BF_MED_MINB) k_small(CountA
     pf.mark(0);
     // ---- the current start
     units_write<NT, P, SM::UCAP>(ss.u, sr.lo, sr.len);
+    cs.nk = min(cs.wl, key_range<ORIENT>(st.s, a.n_u, a.n));
     pf.mark(1);
     uint64_t lsum = 0;
     bool hashed = false;
@@ -896,7 +1075,7 @@ template <int NT, uint32_t WIN, uint32_t CAP, uint32_t LCAP, int P, int G, int U
 struct HeavySmemT {
   static constexpr uint32_t UCAP = CAP / P + NT;
   Units<NT, UCAP> u;
-  uint32_t win[WIN];
+  alignas(16) uint32_t win[WIN];
   uint32_t list[LCAP];
 };
 // split starts whose key ranges all fit DENSE_MAX_KEYS (c4: 30K items) are
@@ -936,6 +1115,7 @@ __global__ void __launch_bounds__(NT, SB == 4 ? 4 : BF_BIG_MINB) k_big(CountArgs
     const uint32_t it = dealt(a, hs.u.item);
     if (it == EMPTY) break;
     const Start st = load_start<ORIENT>(a, it);
+    cs.nk = min(cs.wl, key_range<ORIENT>(st.s, a.n_u, a.n));
     const uint64_t base = __ldg(a.wpre + st.j0);
     const uint64_t w = __ldg(a.wpre + st.j1) - base;
     const bool single = w <= cap && st.j1 - st.j0 <= (uint32_t)NT;
@@ -947,6 +1127,7 @@ __global__ void __launch_bounds__(NT, SB == 4 ? 4 : BF_BIG_MINB) k_big(CountArgs
       __syncthreads();
       const uint32_t cnt = hs.u.lcnt;
       list_finalize<MODE, true, NT>(a, cs, st.kbase, cnt, hs.list, LCAP, olist, lsum);
+      if constexpr (HeavyStore::kScan) cs.template scan_finalize<MODE, NT>(a, st.kbase, false, lsum, pair_acc);
       if (tid == 0) pair_acc += cnt;
       __syncthreads();
       if (MODE != MODE_TOTAL) {
@@ -957,6 +1138,7 @@ __global__ void __launch_bounds__(NT, SB == 4 ? 4 : BF_BIG_MINB) k_big(CountArgs
         const uint32_t key = list_get<true>(hs.list, LCAP, olist, i);
         cs.zero(key, key - st.kbase);
       }
+      if constexpr (HeavyStore::kScan) cs.template scan_reset<NT>(false);
       __syncthreads();
       if (tid == 0) hs.u.lcnt = 0;
     } else {
