@@ -12,6 +12,7 @@
 #include "bf_internal.h"
 #include "bf_device.cuh"
 #include <algorithm>
+#include <cstring>
 
 namespace {
 
@@ -385,11 +386,20 @@ __global__ void k_order_keys(const uint64_t* __restrict__ wstart, const uint32_t
     const uint32_t b = __popc(__ballot_sync(0xffffffffu, tier == 0));
     const uint32_t c = __popc(__ballot_sync(0xffffffffu, tier == 1));
     const uint32_t kmax = __reduce_max_sync(0xffffffffu, kr);
+    // the most wedges of a heavy start (the host skips the split plan's
+    // readback when no start can exceed the split threshold)
+    uint64_t wh = 0;
+    if (b) {
+      wh = tier == 0 ? w : 0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) wh = max(wh, (uint64_t)__shfl_xor_sync(0xffffffffu, wh, o));
+    }
     if ((threadIdx.x & 31) == 0) {
       if (a) atomicAdd(&cnts[0], a);
       if (b) atomicAdd(&cnts[1], b);
       if (c) atomicAdd(&cnts[2], c);
       if (kmax) atomicMax(&cnts[3], kmax);
+      if (wh) atomicMax((unsigned long long*)(cnts + 4), (unsigned long long)wh);
     }
   }
 }
@@ -429,7 +439,7 @@ __global__ void k_compact2(const uint32_t* __restrict__ flag, const uint32_t* __
 
 }  // namespace
 
-static bf_status plan_split(bf_graph* g);
+static bf_status plan_split(bf_graph* g, uint64_t wmax);
 
 bf_status graph_ingest(bf_graph* g, const uint32_t* edges) {
   cudaStream_t s = g->stream;
@@ -695,9 +705,10 @@ bf_status graph_plan(bf_graph* g) {
   uint32_t* k0 = (uint32_t*)g->tmp_a.p + n1 + 16;
   uint32_t* v0 = g->tmp_f.as<uint32_t>();  // src no longer needed
   uint32_t* k1 = g->tmp_c.as<uint32_t>();  // reused after compaction
-  uint32_t* cnts = (uint32_t*)(g->tmp_b.as<char>() + 64);  // [0]=nz [1]=tier 0 [2]=tier 1 [3]=max heavy key range
+  // [0]=nz [1]=tier 0 [2]=tier 1 [3]=max heavy key range [4..5]=max heavy wedges (u64)
+  uint32_t* cnts = (uint32_t*)(g->tmp_b.as<char>() + 64);
   g->order.ensure(n1 * 4);
-  CUDA_TRY(cudaMemsetAsync(cnts, 0, 16, s));
+  CUDA_TRY(cudaMemsetAsync(cnts, 0, 24, s));
   if (n) {
     k_order_keys<<<grid_for(n, g->sms), TPB, 0, s>>>(g->wstart.as<uint64_t>(), g->off.as<uint32_t>(),
                                                       g->hi.as<uint32_t>(), g->orient, n, tr, nzf, key, cnts);
@@ -709,9 +720,9 @@ bf_status graph_plan(bf_graph* g) {
     KERNEL_CHECK(g);
   }
   uint64_t host = 0;
-  uint32_t hc[4], hflag = 0;
+  uint32_t hc[6], hflag = 0;
   CUDA_TRY(cudaMemcpyAsync(&host, dW, 8, cudaMemcpyDeviceToHost, s));
-  CUDA_TRY(cudaMemcpyAsync(hc, cnts, 16, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaMemcpyAsync(hc, cnts, 24, cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaMemcpyAsync(&hflag, g->dflag.p, 4, cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaStreamSynchronize(s));
   if (hflag & 2u) { bf_set_error("duplicate edge"); return BF_EDUP; }
@@ -729,14 +740,16 @@ bf_status graph_plan(bf_graph* g) {
     KERNEL_CHECK(g);
   }
   g->heavy_keys = hc[3] + 1;  // key offsets of heavy starts are < this
-  return plan_split(g);
+  uint64_t wmax;
+  memcpy(&wmax, hc + 4, 8);
+  return plan_split(g, wmax);
 }
 
 // Split starts: heavy starts whose wedges exceed the threshold (a share of W
 // that one CTA would take much longer than the rest of the kernel to finish)
 // are cut into pieces of about threshold/2 wedges.  The heavy tier's items are
 // sorted by wedges, so the split starts are its prefix.
-static bf_status plan_split(bf_graph* g) {
+static bf_status plan_split(bf_graph* g, uint64_t wmax) {
   cudaStream_t s = g->stream;
   g->n_split = 0;
   g->split_batches.clear();
@@ -744,7 +757,7 @@ static bf_status plan_split(bf_graph* g) {
   g->split_threshold = std::max<uint64_t>(tmin, g->W / ((uint64_t)g->sms * 8));
   if (g->opt.test_flags & BF_FLAG_NO_SPLIT) g->split_threshold = ~0ull;
   const uint32_t nh = std::min<uint32_t>(g->n_tier[0], kMaxSplit);
-  if (!nh) return BF_OK;
+  if (!nh || wmax <= g->split_threshold) return BF_OK;  // no start to split: no readback, no sync
   std::vector<uint4>& it = g->h_items;
   it.resize(nh);
   CUDA_TRY(cudaMemcpyAsync(it.data(), g->items.p, (size_t)nh * 16, cudaMemcpyDeviceToHost, s));

@@ -997,6 +997,9 @@ __device__ __forceinline__ SlotRegs load_slot(const CountArgs& a, uint32_t j, ui
   return r;
 }
 
+// medium-tier CTAs per SM (register cap 65536 / (128 * MINB)): 8 -> 64 registers
+// (measured on c2: 48 registers 0.04 ms slower, 40 registers 0.15 ms slower;
+// c3 per-edge: 48 or 64 the same)
 #ifndef BF_MED_MINB
 #define BF_MED_MINB 8
 #endif
@@ -1086,13 +1089,20 @@ struct HeavySmemT {
 // than four 256-thread CTAs with a 4096-key window: 7.3 against 5.5 ms.)
 constexpr uint32_t DENSE_MAX_KEYS = 40960;
 
+// heavy-tier CTAs per SM: the register cap 65536 / (256 * MINB) against the
+// latency of the N(y) reads.  Measured (wedge kernels, c2 vertex / c3 edge /
+// c4 vertex): 64 registers 5.63 / 85.4 / 12.6 ms; 48 (MINB 5) 5.59 / 77.2;
+// 40 (MINB 6) 5.39 / 91.3 -- so 40 registers for vertex and total counts, 48
+// for per-edge counts (more live state per wedge).  SB == 4 (short-segment
+// graphs: c4) keeps four CTAs per SM (14.5 -> 13.2 ms against uncapped).
 #ifndef BF_BIG_MINB
-#define BF_BIG_MINB 1
+#define BF_BIG_MINB 6
 #endif
-// SB == 4 (short-segment graphs): capped at 64 registers, four CTAs per SM
-// (measured on c4: 14.5 -> 13.2 ms); SB == 1 uncapped (c2: 6.75 -> 6.63 ms)
+#ifndef BF_BIG_MINB_E
+#define BF_BIG_MINB_E 5
+#endif
 template <int ORIENT, int MODE, int SB, int NT, uint32_t WIN, uint32_t CAP, uint32_t LCAP, int P, int G, int UR>
-__global__ void __launch_bounds__(NT, SB == 4 ? 4 : BF_BIG_MINB) k_big(CountArgs a) {
+__global__ void __launch_bounds__(NT, SB == 4 ? 4 : (MODE == MODE_EDGE ? BF_BIG_MINB_E : BF_BIG_MINB)) k_big(CountArgs a) {
   using SM = HeavySmemT<NT, WIN, CAP, LCAP, P, G, UR>;
   extern __shared__ __align__(16) char sm[];
   SM& hs = *(SM*)sm;
@@ -1456,7 +1466,7 @@ using MedSM = SmallSmem<MED_CFG>;
 #define BF_BIG_CAP 32768
 #endif
 #ifndef BF_BIG_LCAP
-#define BF_BIG_LCAP 4096
+#define BF_BIG_LCAP 1024  // the shared owner list holds only overflow-row keys (SCAN); more spill to global
 #endif
 #ifndef BF_BIG_P
 #define BF_BIG_P 32
