@@ -193,17 +193,17 @@ template <class K>
 __global__ void __launch_bounds__(RS_THREADS) k_rs_upsweep(const K* __restrict__ keys, size_t n, int shift, int bits,
                                                            uint32_t* __restrict__ counts, uint32_t ntiles) {
   __shared__ uint32_t h[RS_WARPS][256];
-  for (int i = threadIdx.x; i < RS_WARPS * 256; i += RS_THREADS) (&h[0][0])[i] = 0;
-  __syncthreads();
   const size_t base = (size_t)blockIdx.x * RS_TILE;
   const int w = threadIdx.x >> 5;
   const uint32_t mask = (1u << bits) - 1u;
   K k[RS_ITEMS];
 #pragma unroll
-  for (int i = 0; i < RS_ITEMS; i++) {
+  for (int i = 0; i < RS_ITEMS; i++) {  // loads in flight across the counter clear and its barrier
     const size_t idx = base + (size_t)i * RS_THREADS + threadIdx.x;
     k[i] = idx < n ? keys[idx] : (K)0;
   }
+  for (int i = threadIdx.x; i < RS_WARPS * 256; i += RS_THREADS) (&h[0][0])[i] = 0;
+  __syncthreads();
 #pragma unroll
   for (int i = 0; i < RS_ITEMS; i++) {
     const size_t idx = base + (size_t)i * RS_THREADS + threadIdx.x;
@@ -239,7 +239,7 @@ struct RadixDecode {
 };
 
 #ifndef BF_RS_MINB
-#define BF_RS_MINB 4  // measured on c2: 1 -> 4 CTAs per SM takes the rank step 2.62 -> 2.50 ms
+#define BF_RS_MINB 5  // measured on c2: 1 -> 4 CTAs per SM takes the rank step 2.62 -> 2.50 ms; 5: c4 step -0.4 ms
 #endif
 template <class K, bool VALS>
 __global__ void __launch_bounds__(RS_THREADS, BF_RS_MINB) k_rs_downsweep(const K* __restrict__ kin, const uint32_t* __restrict__ vin,
@@ -253,20 +253,20 @@ __global__ void __launch_bounds__(RS_THREADS, BF_RS_MINB) k_rs_downsweep(const K
   __shared__ uint32_t wt[32];
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const uint32_t mask = (1u << bits) - 1u;
-  for (int i = tid; i < RS_WARPS * 64; i += RS_THREADS) reinterpret_cast<uint4*>(&wcnt[0][0])[i] = make_uint4(0, 0, 0, 0);
-  goff[tid] = (uint32_t)tid <= mask ? offs[(size_t)tid * ntiles + blockIdx.x] : 0u;
-  __syncthreads();
   const size_t tbase = (size_t)blockIdx.x * RS_TILE;
   K key[RS_ITEMS];
   uint32_t val[RS_ITEMS];
   uint32_t rk[RS_ITEMS];
 #pragma unroll
-  for (int r = 0; r < RS_ITEMS; r++) {  // all loads in flight before the ranking
-    size_t idx = tbase + (size_t)w * RS_WARP_SPAN + r * 32 + lane;
+  for (int r = 0; r < RS_ITEMS; r++) {  // all loads in flight before the ranking (and before the
+    size_t idx = tbase + (size_t)w * RS_WARP_SPAN + r * 32 + lane;  // digit-offset load and barrier)
     bool valid = idx < n;
     key[r] = valid ? kin[idx] : (K)0;
     if (VALS) val[r] = valid ? vin[idx] : 0u;
   }
+  for (int i = tid; i < RS_WARPS * 64; i += RS_THREADS) reinterpret_cast<uint4*>(&wcnt[0][0])[i] = make_uint4(0, 0, 0, 0);
+  goff[tid] = (uint32_t)tid <= mask ? offs[(size_t)tid * ntiles + blockIdx.x] : 0u;
+  __syncthreads();
 #pragma unroll
   for (int r = 0; r < RS_ITEMS; r++) {
     size_t idx = tbase + (size_t)w * RS_WARP_SPAN + r * 32 + lane;
