@@ -106,8 +106,10 @@ typedef enum { BF_ORIENT_AUTO = 0, BF_ORIENT_LOW = 1, BF_ORIENT_HIGH = 2 } bf_or
                                          more wedges takes the multi-chunk path; the
                                          split threshold drops to 256 wedges            */
 #define BF_FLAG_NO_SPLIT        0x40u /* never split a start across CTAs                */
-#define BF_FLAG_UNPACKED_SORT   0x80u /* no effect since round 2: every slot-sort record
-                                         is one u64 key (kept for source compatibility)  */
+#define BF_FLAG_UNPACKED_SORT   0x80u /* the slot sort's V-half records carry the twin's
+                                         U position (the form taken when bits(|U|) +
+                                         2 bits(|V|) > 64, e.g. configs 3 and 5) instead
+                                         of (u, index of v in N(u))                     */
 #define BF_FLAG_NO_DENSE_ROW    0x100u /* never count split pieces in a whole-key-range
                                          shared row (taken when every heavy start has at
                                          most 40960 same-side keys, e.g. config 4)       */

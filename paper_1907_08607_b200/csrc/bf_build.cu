@@ -639,12 +639,14 @@ bf_status graph_rank(bf_graph* g, int kind) {
     uint32_t* src = g->tmp_f.as<uint32_t>();
     uint32_t* nbr = g->nbr.as<uint32_t>();
     // U half over Bu + Bv bits; its last pass lays out the V half's records
-    // (v field, U position), already in descending-u order, so the V half sorts
-    // over its v field only and its last pass writes both twins' pos (Alg. 1
-    // l.5-6).  Every record is one u64 (Bu + Bv <= 64, Bv + Be <= 63).
-    radix_sort_slots_u(k0, k1, m, Bu, Bv, Be, n, nbr, src, k0 + m, g->n_u, tmp, s, L);
-    radix_sort_slots_v(k0 + m, k1 + m, m, Bv, Be, g->n_u, nbr + m, src + m, g->pos.as<uint32_t>(),
-                       g->off.as<uint32_t>(), src, tmp, s, L);
+    // (v field, U position) -- or, in carry form (Bu + 2 Bv <= 64), (v, u, index
+    // of v in N(u)) -- already in descending-u order, so the V half sorts over
+    // its v field only and its last pass writes both twins' pos (Alg. 1 l.5-6).
+    // Every record is one u64 (Bu + Bv <= 64, Bv + Be <= 63).
+    const bool carry = Bu + 2 * Bv <= 64 && !(g->opt.test_flags & BF_FLAG_UNPACKED_SORT);
+    radix_sort_slots_u(k0, k1, m, Bu, Bv, Be, n, nbr, src, k0 + m, g->n_u, g->off.as<uint32_t>(), carry, tmp, s, L);
+    radix_sort_slots_v(k0 + m, k1 + m, m, Bu, Bv, Be, g->n_u, nbr + m, src + m, g->pos.as<uint32_t>(),
+                       g->off.as<uint32_t>(), src, carry, tmp, s, L);
   }
   if (n) {
     k_hi<<<grid_for(n, g->sms), TPB, 0, s>>>(g->nbr.as<uint32_t>(), g->off.as<uint32_t>(), g->rkey.as<uint64_t>(), n,

@@ -98,11 +98,14 @@ int radix_sort_u64(uint64_t* k0, uint32_t* v0, uint64_t* k1, uint32_t* v1, size_
 // V half: sorts those records on their v field alone (they arrive in
 // descending-u order); writes nbr, src (range-local) and the twin indices
 // pos[q] = p - off[u], pos[p] = q - off[v] (global; usrc = the U half's src).
+// carry (Bu + 2 Bv <= 64): the V records are (v, u, index of v in N(u)) instead
+// of (v, U position), so the V decode gathers nothing from the U half's src.
 void radix_sort_slots_u(uint64_t* k0, uint64_t* k1, size_t m, int Bu, int Bv, int Be, uint64_t n, uint32_t* nbr,
-                        uint32_t* src, uint64_t* vrec, uint64_t nU, void* temp, cudaStream_t s, uint64_t* launches);
-void radix_sort_slots_v(uint64_t* k0, uint64_t* k1, size_t m, int Bv, int Be, uint64_t nU, uint32_t* nbr,
-                        uint32_t* src, uint32_t* pos, const uint32_t* off, const uint32_t* usrc, void* temp,
+                        uint32_t* src, uint64_t* vrec, uint64_t nU, const uint32_t* off, bool carry, void* temp,
                         cudaStream_t s, uint64_t* launches);
+void radix_sort_slots_v(uint64_t* k0, uint64_t* k1, size_t m, int Bu, int Bv, int Be, uint64_t nU, uint32_t* nbr,
+                        uint32_t* src, uint32_t* pos, const uint32_t* off, const uint32_t* usrc, bool carry,
+                        void* temp, cudaStream_t s, uint64_t* launches);
 
 static inline int ceil_log2_u64(uint64_t x) {  // bits needed to hold values < x (x>=1)
   int b = 0;

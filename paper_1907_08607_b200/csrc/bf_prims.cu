@@ -227,15 +227,22 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_upsweep(const K* __restrict__
 // records v_local << Be | p; the twin's source u = usrc[p] (the U half's src),
 // and knowing both twins' positions p and q it writes pos[q] = p - off[u]
 // (index of v in N(u)) and pos[p] = q - off[v] (index of u in N(v)).
+// Carry form (Bu + 2 Bv <= 64: c2, c4): the V record is v_local << (Bu + Bv) |
+// u << Bv | i with i = the index of v in N(u) (< |V|, so Bv bits), written by
+// the U half's decode; the V half's decode then needs no gather of the twin's
+// source (u is in the record) and finds the twin at p = off[u] + i, with pos[q]
+// = i straight from the record.  (Round 1 form: the gather usrc[p] cost c4's V
+// decode most of its 8 ms.)
 struct RadixDecode {
   uint32_t* nbr;         // range-local
   uint32_t* src;         // range-local
   uint32_t* pos;         // V half: global
-  const uint32_t* off;   // V half
-  const uint32_t* usrc;  // V half: the U half's src (global positions < m)
+  const uint32_t* off;   // V half (and the U half's decode in carry form)
+  const uint32_t* usrc;  // V half: the U half's src (global positions < m; not used in carry form)
   uint64_t* tkeys;       // U half: the V half's input records
   uint64_t nbr_last, src_base, pos_base, tm, tbase;
   int B, Be, side;
+  int carry;             // carry form: Bu (> 0), with the U index in B = Bv bits
 };
 
 #ifndef BF_RS_MINB
@@ -320,7 +327,19 @@ __global__ void __launch_bounds__(RS_THREADS, BF_RS_MINB) k_rs_downsweep(const K
         const uint32_t nb = (uint32_t)(dec.nbr_last - (kr & lmask)), sr = (uint32_t)(dec.src_base + (kr >> dec.B));
         dec.nbr[gp] = nb;
         dec.src[gp] = sr;
-        dec.tkeys[dec.tm - 1 - gp] = ((uint64_t)(nb - dec.tbase) << dec.Be) | gp;
+        if (dec.carry)  // v, u, index of v in N(u)
+          dec.tkeys[dec.tm - 1 - gp] = ((uint64_t)(nb - dec.tbase) << (dec.carry + dec.B)) |
+                                       ((uint64_t)sr << dec.B) | (uint32_t)(gp - __ldg(dec.off + sr));
+        else
+          dec.tkeys[dec.tm - 1 - gp] = ((uint64_t)(nb - dec.tbase) << dec.Be) | gp;
+      } else if (dec.carry) {  // V half, carry form: q = pos_base + gp
+        const uint32_t i = (uint32_t)(kr & lmask), u = (uint32_t)((kr >> dec.B) & ((1ull << dec.carry) - 1));
+        const uint32_t v = (uint32_t)(dec.src_base + (kr >> (dec.carry + dec.B)));
+        const uint32_t q = (uint32_t)(dec.pos_base + gp);
+        dec.nbr[gp] = u;
+        dec.src[gp] = v;
+        dec.pos[q] = i;
+        dec.pos[__ldg(dec.off + u) + i] = q - __ldg(dec.off + v);
       } else {  // V half: q = pos_base + gp, twin at U position p
         const uint32_t p = (uint32_t)(kr & emask);
         const uint32_t v = (uint32_t)(dec.src_base + (kr >> dec.Be)), u = __ldg(dec.usrc + p);
@@ -356,7 +375,7 @@ int radix_impl(K* k0, uint32_t* v0, K* k1, uint32_t* v1, size_t n, int begin_bit
   K* ki = k0; K* ko = k1;
   uint32_t* vi = v0; uint32_t* vo = v1;
   int which = 0;
-  const RadixDecode none = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0, 0, 0, 0, 0, 0, 0, 0};
+  const RadixDecode none = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   for (int p = 0, sh = begin_bit; p < passes; p++, sh += bits) {
     RadixDecode d = (dec && p == passes - 1) ? *dec : none;
     k_rs_upsweep<K><<<ntiles, RS_THREADS, 0, s>>>(ki, n, sh, bits, counts, ntiles);
@@ -403,13 +422,19 @@ int radix_sort_u64(uint64_t* k0, uint32_t* v0, uint64_t* k1, uint32_t* v1, size_
   return radix_impl<uint64_t>(k0, v0, k1, v1, n, begin_bit, end_bit, temp, s, launches);
 }
 void radix_sort_slots_u(uint64_t* k0, uint64_t* k1, size_t m, int Bu, int Bv, int Be, uint64_t n, uint32_t* nbr,
-                        uint32_t* src, uint64_t* vrec, uint64_t nU, void* temp, cudaStream_t s, uint64_t* launches) {
-  RadixDecode dec = {nbr, src, nullptr, nullptr, nullptr, vrec, n - 1, 0, 0, m, nU, Bv, Be, 0};
+                        uint32_t* src, uint64_t* vrec, uint64_t nU, const uint32_t* off, bool carry, void* temp,
+                        cudaStream_t s, uint64_t* launches) {
+  RadixDecode dec = {nbr, src, nullptr, off, nullptr, vrec, n - 1, 0, 0, m, nU, Bv, Be, 0, carry ? Bu : 0};
   radix_impl<uint64_t>(k0, nullptr, k1, nullptr, m, 0, Bu + Bv, temp, s, launches, &dec);
 }
-void radix_sort_slots_v(uint64_t* k0, uint64_t* k1, size_t m, int Bv, int Be, uint64_t nU, uint32_t* nbr,
-                        uint32_t* src, uint32_t* pos, const uint32_t* off, const uint32_t* usrc, void* temp,
-                        cudaStream_t s, uint64_t* launches) {
-  RadixDecode dec = {nbr, src, pos, off, usrc, nullptr, 0, nU, m, 0, 0, 0, Be, 1};
+void radix_sort_slots_v(uint64_t* k0, uint64_t* k1, size_t m, int Bu, int Bv, int Be, uint64_t nU, uint32_t* nbr,
+                        uint32_t* src, uint32_t* pos, const uint32_t* off, const uint32_t* usrc, bool carry,
+                        void* temp, cudaStream_t s, uint64_t* launches) {
+  if (carry) {  // records v << (Bu + Bv) | u << Bv | i: sort on the v field
+    RadixDecode dec = {nbr, src, pos, off, nullptr, nullptr, 0, nU, m, 0, 0, Bv, Be, 1, Bu};
+    radix_impl<uint64_t>(k0, nullptr, k1, nullptr, m, Bu + Bv, Bu + 2 * Bv, temp, s, launches, &dec);
+    return;
+  }
+  RadixDecode dec = {nbr, src, pos, off, usrc, nullptr, 0, nU, m, 0, 0, 0, Be, 1, 0};
   radix_impl<uint64_t>(k0, nullptr, k1, nullptr, m, Be, Be + Bv, temp, s, launches, &dec);
 }
