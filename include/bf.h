@@ -116,6 +116,10 @@ typedef enum { BF_ORIENT_AUTO = 0, BF_ORIENT_LOW = 1, BF_ORIENT_HIGH = 2 } bf_or
 #define BF_FLAG_KEY_BUFFER      0x200u /* vertex mode: slot-mode walks always keep their
                                          keys for pass 2 (taken when the average
                                          segment is short, e.g. config 4)                */
+#define BF_FLAG_GRID_JITTER     0x400u /* race stress: every wedge-kernel launch takes a
+                                         pseudo-random grid in [1, its normal grid]
+                                         (a different CTA-to-start mapping and
+                                         interleaving on every call)                     */
 
 typedef struct {
   int device;               /* CUDA ordinal                                           */

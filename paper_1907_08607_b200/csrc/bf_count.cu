@@ -349,6 +349,13 @@ using SmallStore = SmallStoreT<((NT == 32 ? 1 : 2) & BF_SMALL_SCAN) != 0,
 template <bool SCAN>
 struct HeavyStoreT {
   static constexpr bool kScan = SCAN;
+  // kFast: the unit walks test the window bound on the key offset alone (an
+  // empty lane's key EMPTY lands far past every key range) and touch the
+  // window through predicated shared red / loads at ws + 4 kk, so the common
+  // path has no branch; only overflow-row keys take one
+  static constexpr bool kFast = SCAN;
+  uint32_t ws;    // shared-space address of win
+  uint32_t sink;  // first of 32 per-lane sink counters after the window (never read)
   uint32_t* win;
   uint32_t* orow;
   uint32_t wl;
@@ -369,6 +376,8 @@ struct HeavyStoreT {
     }
     return atomicAdd(orow + (kk - wl), 1u) == 0u;
   }
+  // overflow-row increment (kk >= wl); true if it took the count 0 -> 1
+  __device__ __forceinline__ bool add_row(uint32_t kk) const { return atomicAdd(orow + (kk - wl), 1u) == 0u; }
   __device__ __forceinline__ uint32_t get(uint32_t, uint32_t kk) const {
     if (__builtin_expect(kk < wl, 1)) return win[kk];
     return __ldcg(orow + (kk - wl));
@@ -410,6 +419,28 @@ struct HeavyStoreT {
   }
 };
 using HeavyStore = HeavyStoreT<BF_BIG_SCAN != 0>;
+
+template <class S, class = void>
+struct FastOf {
+  static constexpr bool v = false;
+};
+template <class S>
+struct FastOf<S, std::void_t<decltype(S::kFast)>> {
+  static constexpr bool v = S::kFast;
+};
+__device__ __forceinline__ void red_shared_u32_at(uint32_t addr) {
+  asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(addr) : "memory");
+}
+// predicated shared-window load at a shared-space address (no branch; the
+// address is never dereferenced when the predicate is off)
+__device__ __forceinline__ uint32_t ld_shared_if(uint32_t addr, uint32_t kk, uint32_t wl) {
+  uint32_t v;
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.lt.u32 p, %1, %2;\n\tmov.u32 %0, 0;\n\t@p ld.shared.u32 %0, [%3];\n\t}"
+               : "=r"(v)
+               : "r"(kk), "r"(wl), "r"(addr)
+               : "memory");
+  return v;
+}
 
 // the key range of start s (same-side rids ranked above s (HIGH) or below it
 // (LOW)): every key offset kk of its wedges is below it
@@ -576,11 +607,12 @@ __device__ __forceinline__ void units_pass1(const CountArgs& a, Units<NT, UCAP>&
       const uint32_t lo = x < nunits ? u.lo[x] : 0u, me = x < nunits ? u.meta[x] : 0u;
       const uint32_t len = UnitMeta<NT>::len(me, x < nunits);
       ps[r] = me & 0xffffu;
+      const uint32_t* pn = a.nbr + lo + gl;  // one address per unit, immediate offsets per key
 #pragma unroll
       for (int it = 0; it < IT; it++) {
         const uint32_t i = gl + it * G;
         BF_CHECK(i >= len || lo + i < a.S);
-        key[r][it] = i < len ? __ldg(a.nbr + (lo + i)) : EMPTY;
+        key[r][it] = i < len ? __ldg(pn + it * G) : EMPTY;
       }
     }
 #pragma unroll
@@ -588,7 +620,26 @@ __device__ __forceinline__ void units_pass1(const CountArgs& a, Units<NT, UCAP>&
 #pragma unroll
       for (int it = 0; it < IT; it++) {
         uint32_t k = key[r][it];
-        if (k != EMPTY) {
+        if constexpr (FastOf<Store>::v && !CACHE) {
+          // window keys: one unconditional shared red (lanes without a window
+          // key hit their own sink counter past the window); overflow-row keys
+          // are flagged and handled after the unit's keys (a real branch)
+          const uint32_t kk = k - kbase;  // EMPTY: far past the key range
+          BF_CHECK(k == EMPTY || kk < cs.wl || kk - cs.wl < cs.lenchk);
+          red_shared_u32_at(cs.ws + 4u * (kk < cs.wl ? kk : cs.sink + (tid & 31u)));
+          if (it == IT - 1) {
+            bool ovf = false;
+#pragma unroll
+            for (int t = 0; t < IT; t++) ovf |= key[r][t] - kbase >= cs.wl && key[r][t] != EMPTY;
+            if (ovf)
+#pragma unroll
+              for (int t = 0; t < IT; t++) {
+                const uint32_t kt = key[r][t], kkt = kt - kbase;
+                if (kkt >= cs.wl && kt != EMPTY && cs.add_row(kkt))
+                  list_push<SPILL>(&u.lcnt, list, lcap, olist, a.olist_len, kt);
+              }
+          }
+        } else if (k != EMPTY) {
           BF_CHECK(k < a.n);
           if constexpr (CACHE) {
             uint32_t ci;
@@ -618,26 +669,46 @@ __device__ __forceinline__ void units_pass2(const CountArgs& a, Units<NT, UCAP>&
   const uint32_t nunits = u.nunits;
   // warp-uniform trip count: the group reduction below is a full-warp shuffle
   for (uint32_t xb = (tid & ~31u) / G; xb < nunits; xb += NG * UR) {
-    uint32_t key[UR][IT], lo[UR], ps[UR], sl[UR];
+    uint32_t key[UR][IT], lo[UR], ps[UR], sl[UR], ln[UR];
 #pragma unroll
     for (int r = 0; r < UR; r++) {
       const uint32_t x = xb + r * NG + (tid & 31) / G;
       const bool act = x < nunits;
       lo[r] = act ? u.lo[x] : 0u;
       const uint32_t me = act ? u.meta[x] : 0u, len = UnitMeta<NT>::len(me, act);
+      ln[r] = len;
       ps[r] = me & 0xffffu;
       sl[r] = UnitMeta<NT>::slot(me);
+      const uint32_t* pn = a.nbr + lo[r] + gl;
 #pragma unroll
       for (int it = 0; it < IT; it++) {
         const uint32_t i = gl + it * G;
         if constexpr (CACHE) key[r][it] = i < len ? (uint32_t)cache[ps[r] + i] : EMPTY;  // counter index
-        else key[r][it] = i < len ? __ldg(a.nbr + (lo[r] + i)) : EMPTY;
+        else key[r][it] = i < len ? __ldg(pn + it * G) : EMPTY;
       }
     }
 #pragma unroll
     for (int r = 0; r < UR; r++) {
       const uint32_t x = xb + r * NG + (tid & 31) / G;
       typename std::conditional<NARROW, uint32_t, uint64_t>::type s = 0;
+      if constexpr (FastOf<Store>::v && !CACHE && MODE == MODE_VERTEX) {
+        // sum d over the lane's keys (predicated window loads; empty lanes
+        // read nothing), then subtract one per key: sum of (d - 1)
+        bool ovf = false;
+#pragma unroll
+        for (int it = 0; it < IT; it++) {
+          const uint32_t k = key[r][it], kk = k - kbase;
+          s += ld_shared_if(cs.ws + 4u * kk, kk, cs.wl);
+          ovf |= kk >= cs.wl && k != EMPTY;
+        }
+        if (ovf)  // overflow-row keys (rare): a real branch, not if-converted per key
+#pragma unroll
+          for (int it = 0; it < IT; it++) {
+            const uint32_t k = key[r][it], kk = k - kbase;
+            if (kk >= cs.wl && k != EMPTY) s += cs.get(k, kk);
+          }
+        s -= ln[r] > gl ? (ln[r] - gl + (uint32_t)G - 1u) / (uint32_t)G : 0u;
+      } else {
 #pragma unroll
       for (int it = 0; it < IT; it++) {
         if (key[r][it] != EMPTY) {
@@ -656,6 +727,7 @@ __device__ __forceinline__ void units_pass2(const CountArgs& a, Units<NT, UCAP>&
           s += c;
           if (MODE == MODE_EDGE && c) red_add_u64(a.acc + (lo[r] + gl + it * G), c);  // edge (y, key)
         }
+      }
       }
 #pragma unroll
       for (int o = 1; o < G; o <<= 1) s += __shfl_xor_sync(FULL, s, o);
@@ -1078,7 +1150,7 @@ template <int NT, uint32_t WIN, uint32_t CAP, uint32_t LCAP, int P, int G, int U
 struct HeavySmemT {
   static constexpr uint32_t UCAP = CAP / P + NT;
   Units<NT, UCAP> u;
-  alignas(16) uint32_t win[WIN];
+  alignas(16) uint32_t win[WIN + 32];  // + the walks' per-lane sink counters
   uint32_t list[LCAP];
 };
 // split starts whose key ranges all fit DENSE_MAX_KEYS (c4: 30K items) are
@@ -1109,6 +1181,8 @@ __global__ void __launch_bounds__(NT, SB == 4 ? 4 : (MODE == MODE_EDGE ? BF_BIG_
   const uint32_t tid = threadIdx.x, lane = tid & 31;
   HeavyStore cs;
   cs.win = hs.win;
+  cs.ws = (uint32_t)__cvta_generic_to_shared(hs.win);
+  cs.sink = WIN;
   cs.orow = a.orow + (size_t)blockIdx.x * a.orow_len;
   cs.wl = min(a.win, WIN);
   cs.lenchk = a.orow_len;
@@ -1617,6 +1691,17 @@ void row_pool_free(int dev) {
 
 namespace {
 
+// BF_FLAG_GRID_JITTER: a pseudo-random grid in [1, grid] (splitmix64 of the
+// graph's launch draw), so repeated calls map starts to CTAs differently
+int jitter_grid(bf_graph* g, int grid) {
+  if (!(g->opt.test_flags & BF_FLAG_GRID_JITTER) || grid <= 1) return grid;
+  uint64_t z = (++g->jitter) * 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  z ^= z >> 31;
+  return 1 + (int)(z % (uint64_t)grid);
+}
+
 template <int ORIENT, int MODE>
 void launch_tiers(bf_graph* g, CountArgs a, const uint32_t tier[4], uint32_t* queues, cudaStream_t s) {
   const int sms = g->sms;
@@ -1634,8 +1719,8 @@ void launch_tiers(bf_graph* g, CountArgs a, const uint32_t tier[4], uint32_t* qu
       auto k1 = dense ? k_split_walk<ORIENT, MODE, false, true, SP_NT_WIDE> : k_split_walk<ORIENT, MODE, false, false, SP_NT>;
       const int nt1 = dense ? SP_NT_WIDE : SP_NT;
       const size_t smem = dense ? sizeof(SplitSmemT<SP_NT_WIDE>::U) + (size_t)a.dwin * 4 : sizeof(SplitSmemT<SP_NT>);
-      const int grid = sms * occupancy(k1, nt1, smem);
-      const int fgrid = (int)std::min<uint32_t>(b.s1 - b.s0, (uint32_t)sms * 8);
+      const int grid = jitter_grid(g, sms * occupancy(k1, nt1, smem));
+      const int fgrid = jitter_grid(g, (int)std::min<uint32_t>(b.s1 - b.s0, (uint32_t)sms * 8));
       CUDA_TRY(cudaMemsetAsync(queues + 4, 0, 8, s));
       a.queue = queues + 4;
       k1<<<grid, nt1, smem, s>>>(a, sa);
@@ -1647,7 +1732,7 @@ void launch_tiers(bf_graph* g, CountArgs a, const uint32_t tier[4], uint32_t* qu
         auto k2 = dense ? k_split_walk<ORIENT, MODE, true, true, SP_NT_WIDE> : k_split_walk<ORIENT, MODE, true, false, SP_NT_WIDE>;
         const size_t smem2 = sizeof(SplitSmemT<SP_NT_WIDE>::U) + (dense ? (size_t)a.dwin * 4 : 0);
         a.queue = queues + 5;
-        k2<<<sms * occupancy(k2, SP_NT_WIDE, smem2), SP_NT_WIDE, smem2, s>>>(a, sa);
+        k2<<<jitter_grid(g, sms * occupancy(k2, SP_NT_WIDE, smem2)), SP_NT_WIDE, smem2, s>>>(a, sa);
         KERNEL_CHECK(g);
         k_split_clear<ORIENT><<<fgrid, 256, 0, s>>>(a, sa);
         KERNEL_CHECK(g);
@@ -1666,6 +1751,7 @@ void launch_tiers(bf_graph* g, CountArgs a, const uint32_t tier[4], uint32_t* qu
     const size_t row_bytes = (a.orow_len + a.olist_len) * 4;
     RowPool& pool = row_pool(g->device);
     grid = (int)std::max<size_t>(1, std::min<size_t>((size_t)grid, g->pool_budget / row_bytes));
+    grid = jitter_grid(g, grid);
     // rows (kept zero) and lists (scratch) are separate allocations, so a later
     // launch with another grid never finds list garbage inside its rows
     const size_t need_rows = (size_t)grid * a.orow_len * 4, need_lists = (size_t)grid * a.olist_len * 4;
@@ -1693,7 +1779,7 @@ void launch_tiers(bf_graph* g, CountArgs a, const uint32_t tier[4], uint32_t* qu
   }
   if (tier[2] > tier[1]) {  // medium
     auto k = k_small<ORIENT, MODE, MED_CFG>;
-    const int grid = sms * occupancy(k, BF_MEDIUM_MAX_SLOTS, sizeof(MedSM));
+    const int grid = jitter_grid(g, sms * occupancy(k, BF_MEDIUM_MAX_SLOTS, sizeof(MedSM)));
     a.t0 = tier[1]; a.t1 = tier[2]; a.queue = queues + 1;
     k<<<grid, BF_MEDIUM_MAX_SLOTS, sizeof(MedSM), s>>>(a);
     KERNEL_CHECK(g);
@@ -1703,7 +1789,7 @@ void launch_tiers(bf_graph* g, CountArgs a, const uint32_t tier[4], uint32_t* qu
 #ifndef BF_WARP_BLOCKS
 #define BF_WARP_BLOCKS 64
 #endif
-    const int grid = sms * std::min(occupancy(k, 32, sizeof(WarpSM)), BF_WARP_BLOCKS);
+    const int grid = jitter_grid(g, sms * std::min(occupancy(k, 32, sizeof(WarpSM)), BF_WARP_BLOCKS));
     a.t0 = tier[2]; a.t1 = tier[3]; a.queue = queues + 2;
     k<<<grid, 32, sizeof(WarpSM), s>>>(a);
     KERNEL_CHECK(g);

@@ -135,6 +135,7 @@ struct bf_graph {
   bool broken = false;  // after a CUDA/NCCL error
   bool attached = false;  // holds a device_attach reference
   uint64_t launches = 0;
+  uint64_t jitter = 0;   // BF_FLAG_GRID_JITTER: launches drawn so far
 
   uint32_t n_u = 0, n_v = 0;
   uint64_t n = 0, m = 0;

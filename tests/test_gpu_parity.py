@@ -355,6 +355,31 @@ def test_random_graphs_random_paths(bf, seed):
     assert_same(got, ref, f"seed {seed} flags {f:#x} {rank}/{orient} {opts}")
 
 
+@pytest.mark.parametrize("k,scale,rank,flags", [
+    (3, 0.02, "approx_degree", 0),
+    (4, 0.01, "degree", 0x20),         # SMALL_CHUNK: split starts, multi-chunk heavy starts
+    (2, 0.02, "degree", 0x4 | 0x200),  # SMALL_WINDOW + KEY_BUFFER: hash / global-row / slot paths
+])
+def test_race_stress_grid_jitter(bf, k, scale, rank, flags):
+    """Race stress (a racecheck stand-in: compute-sanitizer is not on the pool):
+    every wedge-kernel launch takes a pseudo-random grid (BF_FLAG_GRID_JITTER),
+    so each repetition maps starts to CTAs and interleaves the shared-memory
+    CAS hash, owner lists, window resets and global rows differently; every
+    repetition and mode must stay bit-exact with the oracle."""
+    g = bfgen.config_graph(k, scale)
+    ref = oracle.count(g.n_u, g.n_v, g.edges)
+    f = flags | bf.BF_FLAG_GRID_JITTER
+    for orient in ORIENTS:
+        with bf.ButterflyGraph(g.n_u, g.n_v, g.edges, rank=rank, orient=orient, test_flags=f) as bg:
+            for rep in range(4):
+                ctx = f"c{k} {orient} rep {rep}"
+                assert bg.total() == ref["total"], ctx
+                bu, bv_, t = bg.vertex()
+                assert t == ref["total"] and np.array_equal(bu, ref["b_u"]) and np.array_equal(bv_, ref["b_v"]), ctx
+                be, t = bg.edge()
+                assert t == ref["total"] and np.array_equal(be, ref["b_e"]), ctx
+
+
 def test_nccl_bootstrap_single_rank(bf):
     """The multi-GPU bootstrap on one GPU: NCCL loads at run time, a 1-rank
     communicator is created from the 128-byte id and destroyed."""

@@ -40,6 +40,12 @@ def main():
   for rep in range(4):
       for mode in ("total", "vertex", "edge"):
           cases.append(dict(g=["cfg", 3, 0.02], mode=mode, flags=[], orient="high", rank="approx_degree", rep=rep))
+  # race stress under the bounds-checking build: pseudo-random grids per launch
+  for rep in range(3):
+      for gspec, rank in ((["cfg", 3, 0.02], "approx_degree"), (["cfg", 4, 0.01], "degree")):
+          for mode in ("total", "vertex", "edge"):
+              for flags in (["GRID_JITTER"], ["GRID_JITTER", "SMALL_CHUNK"], ["GRID_JITTER", "SMALL_WINDOW"]):
+                  cases.append(dict(g=gspec, mode=mode, flags=flags, orient="high", rank=rank, rep=rep))
   for c in cases:
       try:
           r = subprocess.run([sys.executable, "-c", CHILD, json.dumps(c)], capture_output=True, text=True, timeout=180)
