@@ -510,7 +510,8 @@ __device__ __forceinline__ void cta_sync() {
 // write the units of one slot segment [lo, lo+L) (thread t), then barrier
 template <int NT, int P, uint32_t UCAP>
 __device__ __forceinline__ void units_write(Units<NT, UCAP>& u, uint32_t lo, uint32_t L) {
-  static_assert(P <= 32 && (P & (P - 1)) == 0, "unit length is packed in 5 bits");
+  static_assert((P <= 32 || (!UnitMeta<NT>::WIDE && P <= 128)) && (P & (P - 1)) == 0,
+                "unit length is packed in 5 bits (wide CTAs) or 8 bits");
   constexpr uint32_t LP = 31 - __builtin_clz(P);
   const uint32_t nu = (L + P - 1) >> LP;
   uint32_t total;
@@ -708,6 +709,27 @@ __device__ __forceinline__ void units_pass2(const CountArgs& a, Units<NT, UCAP>&
             if (kk >= cs.wl && k != EMPTY) s += cs.get(k, kk);
           }
         s -= ln[r] > gl ? (ln[r] - gl + (uint32_t)G - 1u) / (uint32_t)G : 0u;
+      } else if constexpr (FastOf<Store>::v && !CACHE && MODE == MODE_EDGE) {
+        uint32_t d[IT];
+        bool ovf = false;
+#pragma unroll
+        for (int it = 0; it < IT; it++) {
+          const uint32_t k = key[r][it], kk = k - kbase;
+          d[it] = ld_shared_if(cs.ws + 4u * kk, kk, cs.wl);
+          ovf |= kk >= cs.wl && k != EMPTY;
+        }
+        if (ovf)
+#pragma unroll
+          for (int it = 0; it < IT; it++) {
+            const uint32_t k = key[r][it], kk = k - kbase;
+            if (kk >= cs.wl && k != EMPTY) d[it] = cs.get(k, kk);
+          }
+#pragma unroll
+        for (int it = 0; it < IT; it++) {
+          const uint32_t c = d[it] ? d[it] - 1u : 0u;  // empty lanes read d = 0
+          s += c;
+          if (c) red_add_u64(a.acc + (lo[r] + gl + it * G), c);  // edge (y, key)
+        }
       } else {
 #pragma unroll
       for (int it = 0; it < IT; it++) {
@@ -1542,15 +1564,29 @@ using MedSM = SmallSmem<MED_CFG>;
 #ifndef BF_BIG_LCAP
 #define BF_BIG_LCAP 1024  // the shared owner list holds only overflow-row keys (SCAN); more spill to global
 #endif
+// units of P wedges, UR per lane group in flight.  Vertex and total counts:
+// P = 64, one unit (8 keys per lane) -- half the unit-table work of P = 32,
+// UR = 2 for the same keys in flight (measured, wedge kernels: c2 5.13 ->
+// 5.10 ms, c3 vertex 77.2 -> 63.2, c4 11.8 -> 11.5; P = 128: c2 6.09, c3
+// 76.3; P = 64 with UR = 2: c2 5.45); per-edge counts keep P = 32 with UR = 3
+// (c3 edge 72.1 ms; UR = 2 73.0, P = 64 74.5)
 #ifndef BF_BIG_P
-#define BF_BIG_P 32
+#define BF_BIG_P 64
 #endif
 #ifndef BF_BIG_UR
-#define BF_BIG_UR 2
+#define BF_BIG_UR 1
+#endif
+#ifndef BF_BIG_P_E
+#define BF_BIG_P_E 32
+#endif
+#ifndef BF_BIG_UR_E
+#define BF_BIG_UR_E 3
 #endif
 #define BIG_CFG BF_BIG_NT, BF_BIG_WIN, BF_BIG_CAP, BF_BIG_LCAP, BF_BIG_P, BF_BIG_G, BF_BIG_UR
+#define BIG_CFG_E BF_BIG_NT, BF_BIG_WIN, BF_BIG_CAP, BF_BIG_LCAP, BF_BIG_P_E, BF_BIG_G, BF_BIG_UR_E
 constexpr uint64_t HV_WIN_KEYS = BF_BIG_WIN;  // BIG_CFG's window
 using BigSM = HeavySmemT<BIG_CFG>;
+using BigSME = HeavySmemT<BIG_CFG_E>;
 static_assert(BF_WARP_MAX_SLOTS == 32, "warp tier: one slot per lane");
 // tuning-macro consistency (a violation would reach __trap or wrap a counter):
 // every distinct hashed key of a small-tier start fits its hash (distinct keys
@@ -1740,9 +1776,10 @@ void launch_tiers(bf_graph* g, CountArgs a, const uint32_t tier[4], uint32_t* qu
     }
   }
   if (tier[1] > tier[0] + g->n_split) {  // heavy
-    auto k = a.short_segs ? k_big<ORIENT, MODE, 4, BIG_CFG> : k_big<ORIENT, MODE, 1, BIG_CFG>;
+    auto k = MODE == MODE_EDGE ? (a.short_segs ? k_big<ORIENT, MODE, 4, BIG_CFG_E> : k_big<ORIENT, MODE, 1, BIG_CFG_E>)
+                               : (a.short_segs ? k_big<ORIENT, MODE, 4, BIG_CFG> : k_big<ORIENT, MODE, 1, BIG_CFG>);
     const int nt = BF_BIG_NT;
-    const size_t smem = sizeof(BigSM);
+    const size_t smem = MODE == MODE_EDGE ? sizeof(BigSME) : sizeof(BigSM);
     int grid = sms * occupancy(k, nt, smem);
     // one overflow row + touched list per CTA, from the device's row pool
     // (rows are kept zero by the owners' resets, so a clean pool is reused
