@@ -120,6 +120,10 @@ typedef enum { BF_ORIENT_AUTO = 0, BF_ORIENT_LOW = 1, BF_ORIENT_HIGH = 2 } bf_or
                                          pseudo-random grid in [1, its normal grid]
                                          (a different CTA-to-start mapping and
                                          interleaving on every call)                     */
+#define BF_FLAG_HUB_POS         0x800u /* ranked CSR build: always rank the U-side twin
+                                         positions of up to 256 hub items in slot order
+                                         (taken when m >= 2^25 and those items hold at
+                                         least a quarter of the slots, e.g. config 4)    */
 
 typedef struct {
   int device;               /* CUDA ordinal                                           */

@@ -32,7 +32,7 @@ BF_ORIENT_AUTO, BF_ORIENT_LOW, BF_ORIENT_HIGH = 0, 1, 2
 ORIENTS = {"auto": BF_ORIENT_AUTO, "low": BF_ORIENT_LOW, "high": BF_ORIENT_HIGH}
 BF_FLAG_FORCE_WARP, BF_FLAG_FORCE_CTA, BF_FLAG_SMALL_WINDOW, BF_FLAG_FORCE_DENSE = 0x1, 0x2, 0x4, 0x10
 BF_FLAG_SMALL_CHUNK, BF_FLAG_NO_SPLIT, BF_FLAG_UNPACKED_SORT, BF_FLAG_NO_DENSE_ROW = 0x20, 0x40, 0x80, 0x100
-BF_FLAG_KEY_BUFFER, BF_FLAG_GRID_JITTER = 0x200, 0x400
+BF_FLAG_KEY_BUFFER, BF_FLAG_GRID_JITTER, BF_FLAG_HUB_POS = 0x200, 0x400, 0x800
 
 
 class bf_options(ctypes.Structure):

@@ -17,6 +17,12 @@
 namespace {
 
 constexpr int TPB = 256;
+// hub twin positions (hub_pos): from this many edges on the U half's pos array (4m bytes) no
+// longer sits in L2, and the V decode's scatter into it becomes DRAM read-modify-writes
+#ifndef BF_HUB_POS_MIN_SLOTS
+#define BF_HUB_POS_MIN_SLOTS (1ull << 25)
+#endif
+constexpr uint64_t kHubPosMinSlots = BF_HUB_POS_MIN_SLOTS;
 inline unsigned grid_for(size_t n, int sms) {
   size_t g = (n + TPB - 1) / TPB;
   size_t cap = (size_t)sms * 32;
@@ -645,8 +651,17 @@ bf_status graph_rank(bf_graph* g, int kind) {
     // Every record is one u64 (Bu + Bv <= 64, Bv + Be <= 63).
     const bool carry = Bu + 2 * Bv <= 64 && !(g->opt.test_flags & BF_FLAG_UNPACKED_SORT);
     radix_sort_slots_u(k0, k1, m, Bu, Bv, Be, n, nbr, src, k0 + m, g->n_u, g->off.as<uint32_t>(), carry, tmp, s, L);
+    // hub twin positions: when the U half's pos array outgrows L2 (or on BF_FLAG_HUB_POS), the U-side
+    // pos of slots that point at hub items is ranked in order instead of scattered by the V decode
+    const uint32_t* hub = nullptr;
+    if (g->n_v && (m >= kHubPosMinSlots || (g->opt.test_flags & BF_FLAG_HUB_POS))) {
+      uint32_t* hb = g->dflag.as<uint32_t>() + 2;
+      hub_select(g->off.as<uint32_t>(), g->n_u, n, m, (g->opt.test_flags & BF_FLAG_HUB_POS) != 0, hb, s, L);
+      hub_pos(nbr, m, hb, g->off.as<uint32_t>(), g->pos.as<uint32_t>(), tmp, s, L);
+      hub = hb;
+    }
     radix_sort_slots_v(k0 + m, k1 + m, m, Bu, Bv, Be, g->n_u, nbr + m, src + m, g->pos.as<uint32_t>(),
-                       g->off.as<uint32_t>(), src, carry, tmp, s, L);
+                       g->off.as<uint32_t>(), src, carry, hub, tmp, s, L);
   }
   if (n) {
     k_hi<<<grid_for(n, g->sms), TPB, 0, s>>>(g->nbr.as<uint32_t>(), g->off.as<uint32_t>(), g->rkey.as<uint64_t>(), n,

@@ -105,7 +105,16 @@ void radix_sort_slots_u(uint64_t* k0, uint64_t* k1, size_t m, int Bu, int Bv, in
                         cudaStream_t s, uint64_t* launches);
 void radix_sort_slots_v(uint64_t* k0, uint64_t* k1, size_t m, int Bu, int Bv, int Be, uint64_t nU, uint32_t* nbr,
                         uint32_t* src, uint32_t* pos, const uint32_t* off, const uint32_t* usrc, bool carry,
-                        void* temp, cudaStream_t s, uint64_t* launches);
+                        const uint32_t* hub, void* temp, cudaStream_t s, uint64_t* launches);
+// Hub twin positions (bf_prims.cu): hub_select writes hub = {lo, hi}, the global rid range of up to
+// 256 V vertices at the heavier end of the V side when they hold >= 1/4 of the slots (or force), else
+// {0, 0}; hub_pos writes pos[p] for the U-half slots p whose neighbour is a hub by ranking them in
+// slot order (index of u in N(v) = deg(v) - 1 - earlier U-half slots with the same v); the V half's
+// decode (radix_sort_slots_v with the same hub) skips its scatter for those slots.
+void hub_select(const uint32_t* off, uint32_t nU, uint64_t n, uint64_t m, bool force, uint32_t* hub, cudaStream_t s,
+                uint64_t* launches);
+void hub_pos(const uint32_t* nbr, size_t m, const uint32_t* hub, const uint32_t* off, uint32_t* pos, void* temp,
+             cudaStream_t s, uint64_t* launches);
 
 static inline int ceil_log2_u64(uint64_t x) {  // bits needed to hold values < x (x>=1)
   int b = 0;

@@ -243,6 +243,8 @@ struct RadixDecode {
   uint64_t nbr_last, src_base, pos_base, tm, tbase;
   int B, Be, side;
   int carry;             // carry form: Bu (> 0), with the U index in B = Bv bits
+  const uint32_t* hub;   // V half: {lo, hi} global rids of the hub items whose U-side pos is ranked
+                         // in order (hub_pos) instead of scattered here; nullptr = none
 };
 
 #ifndef BF_RS_MINB
@@ -319,6 +321,7 @@ __global__ void __launch_bounds__(RS_THREADS, BF_RS_MINB) k_rs_downsweep(const K
   if (!VALS && dec.nbr) {  // final pass of the slot sort: decode in place of the key write
     const uint64_t lmask = (1ull << dec.B) - 1;
     const uint64_t emask = (1ull << dec.Be) - 1;
+    const uint32_t hub_lo = dec.hub ? __ldg(dec.hub) : 0u, hub_n = dec.hub ? __ldg(dec.hub + 1) - hub_lo : 0u;
     for (uint32_t i = tid; i < cnt; i += RS_THREADS) {
       const uint64_t kr = (uint64_t)skeys[i];
       const uint32_t d = (uint32_t)(kr >> shift) & mask;
@@ -339,7 +342,7 @@ __global__ void __launch_bounds__(RS_THREADS, BF_RS_MINB) k_rs_downsweep(const K
         dec.nbr[gp] = u;
         dec.src[gp] = v;
         dec.pos[q] = i;
-        dec.pos[__ldg(dec.off + u) + i] = q - __ldg(dec.off + v);
+        if (v - hub_lo >= hub_n) dec.pos[__ldg(dec.off + u) + i] = q - __ldg(dec.off + v);
       } else {  // V half: q = pos_base + gp, twin at U position p
         const uint32_t p = (uint32_t)(kr & emask);
         const uint32_t v = (uint32_t)(dec.src_base + (kr >> dec.Be)), u = __ldg(dec.usrc + p);
@@ -347,7 +350,7 @@ __global__ void __launch_bounds__(RS_THREADS, BF_RS_MINB) k_rs_downsweep(const K
         dec.nbr[gp] = u;
         dec.src[gp] = v;
         dec.pos[q] = p - __ldg(dec.off + u);
-        dec.pos[p] = q - __ldg(dec.off + v);
+        if (v - hub_lo >= hub_n) dec.pos[p] = q - __ldg(dec.off + v);
       }
     }
     return;
@@ -393,6 +396,103 @@ int radix_impl(K* k0, uint32_t* v0, K* k1, uint32_t* v1, size_t n, int begin_bit
   return which;
 }
 
+
+// ---- hub twin positions -------------------------------------------------------
+// The V half's decode scatters pos[off[u] + i] = index of u in N(v): random
+// 4-byte writes over the whole U half (on c4 17 GB of DRAM traffic, 5 ms).  The
+// U half runs in ascending u and N(v) in descending u, so the index of u in
+// N(v) is deg(v) - 1 - (number of earlier U-half slots with the same v): for
+// up to 256 hub items (a contiguous rid range at the heavier end of the V
+// side, chosen on the device when it holds >= 1/4 of the slots) it is a
+// per-tile histogram, a scan and an in-order rank, all coalesced; the decode
+// then skips the scatter for those v.
+constexpr uint32_t HUB_BINS = 256;
+__global__ void k_hub_select(const uint32_t* __restrict__ off, uint32_t nU, uint64_t n, uint64_t m, int force,
+                             uint32_t* __restrict__ hub) {
+  const uint64_t nV = n - nU;
+  const uint32_t h = (uint32_t)(nV < HUB_BINS ? nV : HUB_BINS);
+  const uint64_t lo_sum = (uint64_t)off[nU + h] - off[nU], hi_sum = (uint64_t)off[n] - off[n - h];
+  const bool high = hi_sum >= lo_sum;
+  const uint64_t sum = high ? hi_sum : lo_sum;
+  const bool on = h && (force || sum * 4 >= m);
+  hub[0] = on ? (high ? (uint32_t)(n - h) : nU) : 0u;
+  hub[1] = on ? hub[0] + h : 0u;
+}
+__global__ void __launch_bounds__(RS_THREADS) k_hub_hist(const uint32_t* __restrict__ nbr, size_t m,
+                                                          const uint32_t* __restrict__ hub,
+                                                          uint32_t* __restrict__ counts, uint32_t ntiles) {
+  __shared__ uint32_t h[HUB_BINS];
+  const uint32_t lo = hub[0], nh = hub[1] - lo;
+  if (!nh) return;
+  h[threadIdx.x] = 0;
+  __syncthreads();
+  const size_t base = (size_t)blockIdx.x * RS_TILE;
+#pragma unroll
+  for (int i = 0; i < RS_ITEMS; i++) {
+    const size_t idx = base + (size_t)i * RS_THREADS + threadIdx.x;
+    if (idx < m) {
+      const uint32_t b = nbr[idx] - lo;
+      if (b < nh) atomicAdd(&h[b], 1u);
+    }
+  }
+  __syncthreads();
+  counts[(size_t)threadIdx.x * ntiles + blockIdx.x] = h[threadIdx.x];
+}
+__global__ void __launch_bounds__(RS_THREADS) k_hub_rank(const uint32_t* __restrict__ nbr, size_t m,
+                                                          const uint32_t* __restrict__ hub,
+                                                          const uint32_t* __restrict__ offs, uint32_t ntiles,
+                                                          const uint32_t* __restrict__ off,
+                                                          uint32_t* __restrict__ pos) {
+  __shared__ uint32_t wc[RS_WARPS][HUB_BINS];
+  const uint32_t lo = hub[0], nh = hub[1] - lo;
+  if (!nh) return;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const size_t tbase = (size_t)blockIdx.x * RS_TILE;
+  uint32_t b[RS_ITEMS];
+#pragma unroll
+  for (int r = 0; r < RS_ITEMS; r++) {  // warp w: a contiguous span, in slot order
+    const size_t idx = tbase + (size_t)w * RS_WARP_SPAN + r * 32 + lane;
+    uint32_t x = HUB_BINS;
+    if (idx < m) {
+      x = nbr[idx] - lo;
+      if (x >= nh) x = HUB_BINS;
+    }
+    b[r] = x;
+  }
+  for (int i = tid; i < RS_WARPS * (int)HUB_BINS; i += RS_THREADS) (&wc[0][0])[i] = 0;
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < RS_ITEMS; r++)
+    if (b[r] < HUB_BINS) atomicAdd(&wc[w][b[r]], 1u);
+  __syncthreads();
+  {  // thread tid <-> bin tid: slots of this bin before the tile, then before each warp
+    uint32_t run = offs[(size_t)tid * ntiles + blockIdx.x] - offs[(size_t)tid * ntiles];
+#pragma unroll
+    for (int ww = 0; ww < RS_WARPS; ww++) {
+      const uint32_t c = wc[ww][tid];
+      wc[ww][tid] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < RS_ITEMS; r++) {
+    const size_t idx = tbase + (size_t)w * RS_WARP_SPAN + r * 32 + lane;
+    const uint32_t x = b[r];
+    const unsigned peers = __match_any_sync(0xffffffffu, x);
+    const bool hubv = x < HUB_BINS;
+    const uint32_t before = hubv ? wc[w][x] : 0u;
+    __syncwarp();
+    if (hubv && (peers >> lane) == 1u) wc[w][x] = before + (uint32_t)__popc(peers);
+    __syncwarp();
+    if (hubv) {
+      const uint32_t v = lo + x;
+      const uint32_t rank = before + (uint32_t)__popc(peers & ((1u << lane) - 1u));
+      pos[idx] = __ldg(off + v + 1) - __ldg(off + v) - 1u - rank;
+    }
+  }
+}
+
 }  // namespace
 
 size_t scan_temp_bytes(size_t n) { return scan_levels_elems(n) * 8 + 256; }
@@ -407,6 +507,26 @@ void scan_exclusive_u64(const uint64_t* in, uint64_t* out, size_t n, uint64_t* t
 void scan_exclusive_u32_u64(const uint32_t* in, uint64_t* out, size_t n, uint64_t* total, void* temp,
                             cudaStream_t s, uint64_t* launches) {
   scan_impl<uint32_t, uint64_t>(in, out, n, total, (uint64_t*)temp, s, launches);
+}
+void hub_select(const uint32_t* off, uint32_t nU, uint64_t n, uint64_t m, bool force, uint32_t* hub, cudaStream_t s,
+                uint64_t* launches) {
+  k_hub_select<<<1, 1, 0, s>>>(off, nU, n, m, force ? 1 : 0, hub);
+  (*launches)++;
+  CUDA_TRY(cudaGetLastError());
+}
+void hub_pos(const uint32_t* nbr, size_t m, const uint32_t* hub, const uint32_t* off, uint32_t* pos, void* temp,
+             cudaStream_t s, uint64_t* launches) {
+  if (m == 0) return;
+  const uint32_t ntiles = (uint32_t)((m + RS_TILE - 1) / RS_TILE);
+  uint32_t* counts = (uint32_t*)temp;
+  uint32_t* stemp = counts + (size_t)ntiles * 256 + 64;
+  k_hub_hist<<<ntiles, RS_THREADS, 0, s>>>(nbr, m, hub, counts, ntiles);
+  (*launches)++;
+  CUDA_TRY(cudaGetLastError());
+  scan_impl<uint32_t, uint32_t>(counts, counts, (size_t)ntiles * HUB_BINS, nullptr, stemp, s, launches);
+  k_hub_rank<<<ntiles, RS_THREADS, 0, s>>>(nbr, m, hub, counts, ntiles, off, pos);
+  (*launches)++;
+  CUDA_TRY(cudaGetLastError());
 }
 size_t radix_temp_bytes(size_t n) {
   size_t ntiles = (n + RS_TILE - 1) / RS_TILE;
@@ -424,17 +544,17 @@ int radix_sort_u64(uint64_t* k0, uint32_t* v0, uint64_t* k1, uint32_t* v1, size_
 void radix_sort_slots_u(uint64_t* k0, uint64_t* k1, size_t m, int Bu, int Bv, int Be, uint64_t n, uint32_t* nbr,
                         uint32_t* src, uint64_t* vrec, uint64_t nU, const uint32_t* off, bool carry, void* temp,
                         cudaStream_t s, uint64_t* launches) {
-  RadixDecode dec = {nbr, src, nullptr, off, nullptr, vrec, n - 1, 0, 0, m, nU, Bv, Be, 0, carry ? Bu : 0};
+  RadixDecode dec = {nbr, src, nullptr, off, nullptr, vrec, n - 1, 0, 0, m, nU, Bv, Be, 0, carry ? Bu : 0, nullptr};
   radix_impl<uint64_t>(k0, nullptr, k1, nullptr, m, 0, Bu + Bv, temp, s, launches, &dec);
 }
 void radix_sort_slots_v(uint64_t* k0, uint64_t* k1, size_t m, int Bu, int Bv, int Be, uint64_t nU, uint32_t* nbr,
                         uint32_t* src, uint32_t* pos, const uint32_t* off, const uint32_t* usrc, bool carry,
-                        void* temp, cudaStream_t s, uint64_t* launches) {
+                        const uint32_t* hub, void* temp, cudaStream_t s, uint64_t* launches) {
   if (carry) {  // records v << (Bu + Bv) | u << Bv | i: sort on the v field
-    RadixDecode dec = {nbr, src, pos, off, nullptr, nullptr, 0, nU, m, 0, 0, Bv, Be, 1, Bu};
+    RadixDecode dec = {nbr, src, pos, off, nullptr, nullptr, 0, nU, m, 0, 0, Bv, Be, 1, Bu, hub};
     radix_impl<uint64_t>(k0, nullptr, k1, nullptr, m, Bu + Bv, Bu + 2 * Bv, temp, s, launches, &dec);
     return;
   }
-  RadixDecode dec = {nbr, src, pos, off, usrc, nullptr, 0, nU, m, 0, 0, 0, Be, 1, 0};
+  RadixDecode dec = {nbr, src, pos, off, usrc, nullptr, 0, nU, m, 0, 0, 0, Be, 1, 0, hub};
   radix_impl<uint64_t>(k0, nullptr, k1, nullptr, m, Be, Be + Bv, temp, s, launches, &dec);
 }

@@ -96,7 +96,8 @@ def test_random_small(bf, seed):
                                    "cta+small_window", "small_chunk+small_window", "dense+no_split+small_chunk",
                                    "unpacked_sort", "no_dense_row", "dense+no_dense_row",
                                    "small_chunk+no_dense_row", "dense+small_chunk+no_dense_row", "key_buffer",
-                                   "dense+key_buffer", "dense+small_chunk+key_buffer"])
+                                   "dense+key_buffer", "dense+small_chunk+key_buffer", "hub_pos",
+                                   "hub_pos+unpacked_sort"])
 @pytest.mark.parametrize("orient", ORIENTS)
 def test_forced_paths(bf, flags, orient):
     """T3: every start through one tier; tiny windows force the overflow paths
@@ -122,6 +123,8 @@ def test_forced_paths(bf, flags, orient):
         f |= bf.BF_FLAG_NO_DENSE_ROW  # heavy tier: 4096-key window + global overflow rows
     if "unpacked_sort" in flags:
         f |= bf.BF_FLAG_UNPACKED_SORT  # the c5-size slot sort (key and value arrays)
+    if "hub_pos" in flags:
+        f |= bf.BF_FLAG_HUB_POS  # U-side twin positions of the hub items ranked in slot order
     opts = dict(test_flags=f)
     if flags == "light8":
         opts["test_light_max_wedges"] = 8
@@ -236,6 +239,22 @@ def test_csr_export(bf):
             assert (c["wstart"][rid] == w_ref).all()
 
 
+@pytest.mark.parametrize("g", [("C", 700, 500, 5000, 2.1, 2.1, 9), ("cfg", 4, 0.002), ("cfg", 3, 0.002), ("K", 40, 33)])
+def test_hub_pos_same_csr(bf, g):
+    """BF_FLAG_HUB_POS (the U-side twin positions of the hub items ranked in slot
+    order instead of scattered by the V half's decode) builds the same ranked CSR,
+    array for array, in both slot-sort record forms and under every ranking."""
+    g = bfgen.complete(*g[1:]) if g[0] == "K" else (bfgen.config_graph(*g[1:]) if g[0] == "cfg" else bfgen.chung_lu(*g[1:4], *g[4:6], seed=g[6]))
+    for rank in RANKS:
+        for extra in (0, bf.BF_FLAG_UNPACKED_SORT):
+            with bf.ButterflyGraph(g.n_u, g.n_v, g.edges, rank=rank, test_flags=extra) as bg:
+                a = bg.export_csr()
+            with bf.ButterflyGraph(g.n_u, g.n_v, g.edges, rank=rank, test_flags=extra | bf.BF_FLAG_HUB_POS) as bg:
+                b = bg.export_csr()
+            for k in ("rid_of_gid", "off", "nbr", "pos", "hi", "wstart"):
+                assert np.array_equal(a[k], b[k]), (rank, extra, k)
+
+
 @pytest.mark.parametrize("orient", ORIENTS)
 def test_repeated_graphs_same_process(bf, orient):
     """Library state that outlives a graph (the per-device pool of heavy-tier
@@ -341,7 +360,7 @@ def test_random_graphs_random_paths(bf, seed):
     g = bfgen.chung_lu(n_u, n_v, m, float(rng.uniform(1.8, 2.6)), float(rng.uniform(1.8, 2.6)), seed=seed + 1)
     ref = oracle.count(g.n_u, g.n_v, g.edges)
     names = ["FORCE_WARP", "FORCE_CTA", "FORCE_DENSE", "SMALL_WINDOW", "SMALL_CHUNK", "NO_SPLIT", "UNPACKED_SORT",
-             "NO_DENSE_ROW", "KEY_BUFFER"]
+             "NO_DENSE_ROW", "KEY_BUFFER", "HUB_POS"]
     f = 0
     for nm in names:
         if rng.random() < 0.3:
