@@ -71,7 +71,51 @@ class ClockSampler:
         self.lines = []  # (host arrival time, csv line)
         self.windows = []  # timed regions (host time)
 
+    def _nvml_open(self):
+        """In-process NVML (what nvidia-smi itself reads): a looping nvidia-smi process beside the
+        benchmark stalls the launching thread for milliseconds whenever one of its queries lands
+        inside a step (r02c/r02f: +1.2 to +2.0 ms per c2 step with a second sample in the region),
+        so the same clocks and event reasons are read here from a thread.  BF_CLOCKS=smi selects
+        the nvidia-smi loop."""
+        import pynvml
+        pynvml.nvmlInit()
+        idx = self.idx
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+        if vis:
+            ent = [x.strip() for x in vis.split(",") if x.strip()]
+            if idx < len(ent) and ent[idx].isdigit():
+                idx = int(ent[idx])
+        h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+        smax = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+        pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+        pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+        return pynvml, h, smax
+
+    def _nvml_loop(self, pynvml, h, smax):
+        bits = [pynvml.nvmlClocksEventReasonHwSlowdown, pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+                pynvml.nvmlClocksEventReasonSwThermalSlowdown, pynvml.nvmlClocksEventReasonSwPowerCap]
+        while not self.stop.is_set():
+            try:
+                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                f = [str(self.idx), str(sm), str(smax), "", hex(r)] + ["Active" if r & b else "Not Active" for b in bits]
+                self.lines.append((time.time(), ", ".join(f)))
+            except Exception:
+                pass
+            self.stop.wait(0.05)
+
     def __enter__(self):
+        self.stop = threading.Event()
+        self.source = "nvidia-smi"
+        if os.environ.get("BF_CLOCKS", "nvml") != "smi":
+            try:
+                args = self._nvml_open()
+                self.t = threading.Thread(target=self._nvml_loop, args=args, daemon=True)
+                self.t.start()
+                self.source = "nvml"
+                return self
+            except Exception:
+                pass
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}",
                                           "--format=csv,noheader,nounits", "-lms", "50"],
@@ -91,10 +135,11 @@ class ClockSampler:
 
     def wait_first(self, limit: float = 5.0):
         t = time.time()
-        while self.proc and not self.lines and time.time() - t < limit:
+        while (self.proc or self.source == "nvml") and not self.lines and time.time() - t < limit:
             time.sleep(0.02)
 
     def __exit__(self, *a):
+        self.stop.set()
         if self.proc:
             self.proc.terminate()
             try:
@@ -128,7 +173,7 @@ class ClockSampler:
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
         return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": smax, "reasons": sorted(reasons),
-                "samples": len(sm), "period_ms": 50}
+                "samples": len(sm), "period_ms": 50, "source": self.source}
 
 
 # ----------------------------------------------------------------------------- CPU oracle
